@@ -1,0 +1,393 @@
+// C-ABI host layer (include/tileattn_b200.h): validation with the reference's
+// order and error classes, the plan cache, TMA descriptor encoding and the
+// launch of the sm_100a kernel.  No CPU fallback: every compute call either
+// runs the CUDA kernel or returns an error.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/tileattn_b200.h"
+#include "sdpa_fwd_sm100.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ta_status fail(ta_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+ta_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? TA_ERR_OOM : TA_ERR_CUDA,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Validation — restates types.cpp:80-116 and tiled.cpp:21-35.
+// ---------------------------------------------------------------------------
+bool schedule_ok(const ta_schedule& s) {
+  const bool tm = s.t_m == 16 || s.t_m == 32 || s.t_m == 64 || s.t_m == 128;
+  const bool tn = s.t_n == 16 || s.t_n == 32 || s.t_n == 64 || s.t_n == 128 || s.t_n == 256;
+  return tm && tn && s.stages >= 1 && s.stages <= 4 && (s.layout == 0 || s.layout == 1);
+}
+
+ta_schedule resolve_schedule(ta_schedule s) {
+  if (s.t_m == 0 && s.t_n == 0 && s.stages == 0 && s.layout == 0)
+    return ta_schedule{64, 128, 2, 0};  // TileSchedule{} default (tiled.hpp:30-37)
+  return s;
+}
+
+ta_status validate_common(ta_shape sh, ta_mask_kind mask, const int64_t* valid_len,
+                          ta_schedule sched, int has_scale, double scale, double* eff_scale) {
+  // shape (types.cpp:80-83)
+  if (sh.b < 1 || sh.h < 1 || sh.s < 1 || sh.d < 1)
+    return fail(TA_ERR_INVALID_ARGUMENT, "shape extents must all be >= 1");
+  // mask (types.cpp:99-106)
+  if (mask != TA_MASK_NONE && mask != TA_MASK_CAUSAL && mask != TA_MASK_PADDING)
+    return fail(TA_ERR_INVALID_ARGUMENT, "unknown mask kind");
+  if (mask == TA_MASK_PADDING) {
+    if (valid_len == nullptr)
+      return fail(TA_ERR_INVALID_ARGUMENT, "padding mask needs one valid_len per batch");
+    for (int64_t b = 0; b < sh.b; ++b)
+      if (valid_len[b] < 0 || valid_len[b] > sh.s)
+        return fail(TA_ERR_INVALID_ARGUMENT, "padding valid_len out of [0,S]");
+  }
+  // schedule (tiled.cpp:29-35)
+  if (!schedule_ok(sched))
+    return fail(TA_ERR_UNSUPPORTED, "unsupported schedule: t_m=" + std::to_string(sched.t_m) +
+                                        " t_n=" + std::to_string(sched.t_n) +
+                                        " stages=" + std::to_string(sched.stages));
+  // scale (types.cpp:108-116)
+  if (has_scale) {
+    if (!(scale > 0.0))
+      return fail(TA_ERR_INVALID_ARGUMENT, "effective_scale: explicit scale must be > 0");
+    *eff_scale = scale;
+  } else {
+    *eff_scale = 1.0 / std::sqrt(double(sh.d));
+  }
+  return TA_OK;
+}
+
+ta_status validate_device_support(ta_shape sh, ta_dtype dt, ta_mask_kind mask) {
+  if (dt == TA_F32)
+    return fail(TA_ERR_UNSUPPORTED, "dtype f32 is not a tensor-core input; use f16 or bf16");
+  if (dt != TA_F16 && dt != TA_BF16) return fail(TA_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (sh.d != 64 && sh.d != 128)
+    return fail(TA_ERR_UNSUPPORTED, "head dim " + std::to_string(sh.d) +
+                                        " not supported (D in {64,128})");
+  if (mask != TA_MASK_NONE)
+    return fail(TA_ERR_UNSUPPORTED, "mask kind not yet supported on the sm_100a path");
+  if (sh.s > (int64_t(1) << 30)) return fail(TA_ERR_UNSUPPORTED, "S too large");
+  if (sh.b * sh.h > 65535) return fail(TA_ERR_UNSUPPORTED, "B*H > 65535");
+  return TA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Plan cache: the reference's PlanCache (tiled.cpp:37-70) keyed by
+// (t_m, t_n, D, dtype, causal).  The plan records the executed GPU tiling.
+// ---------------------------------------------------------------------------
+struct Plan {
+  int block_m, block_n, stages, q_tiles, threads;
+};
+
+struct PlanCache {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int64_t, int, int>, std::shared_ptr<const Plan>> plans;
+  std::atomic<uint64_t> hits{0}, constructions{0};
+};
+
+PlanCache& plan_cache() {
+  static PlanCache c;
+  return c;
+}
+
+std::shared_ptr<const Plan> get_plan(const ta_schedule& s, int64_t d, ta_dtype dt, bool causal) {
+  PlanCache& c = plan_cache();
+  const auto key = std::make_tuple(s.t_m, s.t_n, d, int(dt), int(causal));
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.plans.find(key);
+    if (it != c.plans.end()) {
+      c.hits.fetch_add(1, std::memory_order_relaxed);
+      return it->second;
+    }
+  }
+  auto g = ta::fwd_geometry(1, 1);
+  auto plan = std::make_shared<const Plan>(
+      Plan{g.block_m, g.block_n, ta::fwd_ring_slots(int(d)), g.q_tiles_per_cta, g.threads});
+  c.constructions.fetch_add(1, std::memory_order_relaxed);
+  std::lock_guard<std::mutex> lock(c.mu);
+  auto [it, inserted] = c.plans.emplace(key, std::move(plan));
+  return it->second;
+}
+
+// ---------------------------------------------------------------------------
+// TMA descriptors (driver entry point fetched through the runtime, so the
+// library does not link libcuda and loads on GPU-less hosts).
+// ---------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return EncodeTiledFn(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// [BH][rows][cols] 16-bit tensor, boxes of 64 cols (128 B, SWIZZLE_128B) x box_rows.
+ta_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t bh, int64_t rows,
+                    int64_t cols, uint32_t box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(rows), cuuint64_t(bh)};
+  cuuint64_t strides[2] = {cuuint64_t(cols * 2), cuuint64_t(rows * cols * 2)};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return TA_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int device_cc(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return cache[dev] = major * 10 + minor;
+}
+
+ta_status check_device() {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TA_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  if (device_cc(dev) != 100)
+    return fail(TA_ERR_CUDA, "device " + std::to_string(dev) +
+                                 " is not sm_100 (this library carries sm_100a code only)");
+  return TA_OK;
+}
+
+void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh) {
+  if (!st) return;
+  const int64_t bh = sh.b * sh.h;
+  const int64_t q_tiles = (sh.s + p.block_m - 1) / p.block_m;
+  const int64_t kv_tiles = (sh.s + p.block_n - 1) / p.block_n;
+  const auto g = ta::fwd_geometry(sh.s, bh);
+  st->kv_tiles_visited = uint64_t(bh * q_tiles * kv_tiles);
+  st->block_m = p.block_m;
+  st->block_n = p.block_n;
+  st->stages = p.stages;
+  st->q_tiles_per_cta = p.q_tiles;
+  st->ctas = g.ctas;
+  st->threads_per_cta = p.threads;
+  st->reserved = 0;
+}
+
+ta_status run_device(const void* q, const void* k, const void* v, void* o, float* lse,
+                     ta_shape sh, ta_dtype dt, double scale, const Plan& plan, void* stream) {
+  const bool bf16 = dt == TA_BF16;
+  const int64_t bh = sh.b * sh.h;
+  CUtensorMap mq, mk, mv;
+  ta_status st;
+  if ((st = make_tmap(&mq, q, bf16, bh, sh.s, sh.d, 128)) != TA_OK) return st;
+  if ((st = make_tmap(&mk, k, bf16, bh, sh.s, sh.d, 128)) != TA_OK) return st;
+  if ((st = make_tmap(&mv, v, bf16, bh, sh.s, sh.d, 128)) != TA_OK) return st;
+  ta::FwdLaunch L{};
+  L.tmap_q = &mq;
+  L.tmap_k = &mk;
+  L.tmap_v = &mv;
+  L.args.o = o;
+  L.args.lse = lse;
+  L.args.seq_len = int(sh.s);
+  L.args.scale_log2 = float(scale * 1.4426950408889634074);
+  L.bh = bh;
+  L.head_dim = int(sh.d);
+  L.bf16 = bf16;
+  L.stream = stream;
+  (void)plan;
+  cudaError_t e = ta::launch_sdpa_fwd(L);
+  if (e != cudaSuccess) return cuda_fail(e, "sdpa_fwd launch");
+  return TA_OK;
+}
+
+// per-device workspace for the host-buffer entry
+struct Workspace {
+  std::mutex mu;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+Workspace& workspace(int dev) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<Workspace>> ws;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& w = ws[dev];
+  if (!w) w = std::make_unique<Workspace>();
+  return *w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ta_last_error(void) { return g_last_error.c_str(); }
+
+int ta_abi_version(void) { return TA_ABI_VERSION; }
+
+int ta_schedule_supported(ta_schedule sched) { return schedule_ok(sched) ? 1 : 0; }
+
+ta_status ta_effective_scale(int has_scale, double scale, int64_t d, double* out) {
+  if (d < 1) return fail(TA_ERR_INVALID_ARGUMENT, "effective_scale: D must be >= 1");
+  if (has_scale) {
+    if (!(scale > 0.0))
+      return fail(TA_ERR_INVALID_ARGUMENT, "effective_scale: explicit scale must be > 0");
+    if (out) *out = scale;
+    return TA_OK;
+  }
+  if (out) *out = 1.0 / std::sqrt(double(d));
+  return TA_OK;
+}
+
+void ta_plan_cache_stats(uint64_t* hits, uint64_t* constructions) {
+  if (hits) *hits = plan_cache().hits.load();
+  if (constructions) *constructions = plan_cache().constructions.load();
+}
+
+void ta_plan_cache_clear(void) {
+  PlanCache& c = plan_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  c.plans.clear();
+  c.hits = 0;
+  c.constructions = 0;
+}
+
+int ta_device_supported(int device) { return device_cc(device) == 100 ? 1 : 0; }
+
+ta_status ta_sdpa_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                      ta_shape shape, ta_dtype dtype, ta_mask_kind mask,
+                      const int64_t* valid_len, int has_scale, double scale,
+                      ta_schedule sched, void* stream, ta_kernel_stats* stats) {
+  sched = resolve_schedule(sched);
+  double eff = 0.0;
+  ta_status st = validate_common(shape, mask, valid_len, sched, has_scale, scale, &eff);
+  if (st != TA_OK) return st;
+  if (!q || !k || !v || !o) return fail(TA_ERR_INVALID_ARGUMENT, "null tensor pointer");
+  if ((st = validate_device_support(shape, dtype, mask)) != TA_OK) return st;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(TA_ERR_INVALID_ARGUMENT, "q/k/v/o must be 16-byte aligned");
+  if ((st = check_device()) != TA_OK) return st;
+  auto plan = get_plan(sched, shape.d, dtype, mask == TA_MASK_CAUSAL);
+  if ((st = run_device(q, k, v, o, lse, shape, dtype, eff, *plan, stream)) != TA_OK) return st;
+  fill_stats(stats, *plan, shape);
+  return TA_OK;
+}
+
+ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o, float* lse,
+                           ta_shape shape, ta_dtype dtype, ta_mask_kind mask,
+                           const int64_t* valid_len, int has_scale, double scale,
+                           ta_schedule sched, void* stream, ta_kernel_stats* stats) {
+  sched = resolve_schedule(sched);
+  double eff = 0.0;
+  ta_status st = validate_common(shape, mask, valid_len, sched, has_scale, scale, &eff);
+  if (st != TA_OK) return st;
+  if (!q || !k || !v || !o) return fail(TA_ERR_INVALID_ARGUMENT, "null tensor pointer");
+  if ((st = validate_device_support(shape, dtype, mask)) != TA_OK) return st;
+  if ((st = check_device()) != TA_OK) return st;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t n = size_t(shape.b * shape.h * shape.s * shape.d);
+  const size_t tbytes = (n * 2 + 255) & ~size_t(255);
+  const size_t lbytes = lse ? ((size_t(shape.b * shape.h * shape.s) * 4 + 255) & ~size_t(255)) : 0;
+  const size_t need = 4 * tbytes + lbytes;
+  Workspace& ws = workspace(dev);
+  std::lock_guard<std::mutex> lock(ws.mu);
+  if (ws.bytes < need) {
+    if (ws.ptr) cudaFree(ws.ptr);
+    ws.ptr = nullptr;
+    ws.bytes = 0;
+    cudaError_t e = cudaMalloc(&ws.ptr, need);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cuda_fail(e, "workspace cudaMalloc");
+    }
+    ws.bytes = need;
+  }
+  char* base = static_cast<char*>(ws.ptr);
+  void* dq = base;
+  void* dk = base + tbytes;
+  void* dv = base + 2 * tbytes;
+  void* dout = base + 3 * tbytes;
+  float* dl = lse ? reinterpret_cast<float*>(base + 4 * tbytes) : nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(dq, q, n * 2, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(dk, k, n * 2, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(dv, v, n * 2, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "H2D copy");
+  auto plan = get_plan(sched, shape.d, dtype, mask == TA_MASK_CAUSAL);
+  if ((st = run_device(dq, dk, dv, dout, dl, shape, dtype, eff, *plan, stream)) != TA_OK)
+    return st;
+  if ((e = cudaMemcpyAsync(o, dout, n * 2, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "D2H copy");
+  if (lse &&
+      (e = cudaMemcpyAsync(lse, dl, size_t(shape.b * shape.h * shape.s) * 4,
+                           cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "D2H copy");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
+  fill_stats(stats, *plan, shape);
+  return TA_OK;
+}
+
+ta_status ta_debug_umma_gemm(int mode, ta_dtype dtype, const void* a, const void* b, float* d,
+                             void* stream) {
+  if (mode < 0 || mode > 2) return fail(TA_ERR_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
+  if (dtype != TA_F16 && dtype != TA_BF16) return fail(TA_ERR_UNSUPPORTED, "dtype");
+  ta_status st;
+  if ((st = check_device()) != TA_OK) return st;
+  CUtensorMap ma, mb;
+  const bool bf16 = dtype == TA_BF16;
+  if ((st = make_tmap(&ma, a, bf16, 1, 128, 128, 128)) != TA_OK) return st;
+  if ((st = make_tmap(&mb, b, bf16, 1, 128, 128, 128)) != TA_OK) return st;
+  cudaError_t e = ta::launch_umma_selftest(&ma, &mb, a, d, mode, bf16, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "selftest launch");
+  if ((e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream))) != cudaSuccess)
+    return cuda_fail(e, "selftest sync");
+  return TA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,482 @@
+// SDPA forward for B200 (sm_100a): TMA -> 128B-swizzled smem ring -> tcgen05.mma
+// (QK^T and PV, fp32 accumulators in TMEM) with warp-specialised roles and an
+// online softmax in registers (one thread == one query row).
+//
+// Replaces the reference CPU hot path tileattn::sdpa_tiled / run_tiled
+// (reference proj/src/tiled.cpp:119-272, proj/include/tileattn/tiled.hpp:
+// 147-238).  Algorithm per (bh, query block) is the reference's item_body
+// (tiled.cpp:144-221): load Q tile once, stream K/V tiles, score_tile ->
+// mask -> online_update, finalize O = o / l.  Differences are B200-native:
+//   * two 128-row Q tiles per CTA ping-pong on the tensor core (the MMA of
+//     one tile overlaps the softmax of the other);
+//   * scores never leave TMEM except into the softmax registers; P (16-bit)
+//     is written back into the S columns of TMEM and consumed by a TS-MMA;
+//   * exp2 with the softmax scale folded into one FFMA; the running max is
+//     updated lazily (only when it grows by > 2^8), so the O correction in
+//     TMEM is rare (tiled.hpp:212 skips the rescale only when alpha == 1);
+//   * LSE = m + ln(l) is emitted as a second output (the reference computes
+//     m and l but never returns them, tiled.hpp:223-238).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "ptx_sm100.cuh"
+#include "sdpa_fwd_sm100.h"
+
+namespace ta {
+namespace {
+
+constexpr int kBM = 128;        // rows per Q tile (UMMA M)
+constexpr int kBN = 128;        // keys per K/V tile (UMMA N of QK^T, K of PV)
+constexpr int kQTiles = 2;      // Q tiles per CTA (ping-pong)
+constexpr int kThreads = 384;   // 12 warps
+constexpr int kSoftmaxWarp0 = 4;  // warps 4..7 -> Q tile 0, 8..11 -> Q tile 1
+constexpr uint32_t kTmemCols = 512;
+// register split: 4 control warps (TMA, MMA, TMEM alloc, spare) + 8 softmax warps
+constexpr int kRegsControl = 96;
+constexpr int kRegsSoftmax = 200;  // 128*96 + 256*200 <= 64K
+constexpr float kLn2 = 0.69314718055994530942f;
+// lazy rescale threshold in log2 units: exps may reach 2^8 before O is
+// rescaled (fp32 accumulators, 16-bit P: both fine).
+constexpr float kRescaleThreshold = 8.0f;
+
+template <int D>
+struct Cfg {
+  static constexpr int kRegions = D / 64;                   // 128-B swizzle atoms along D
+  static constexpr int kTileBytes = kBM * D * 2;            // one Q / K / V tile
+  static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
+  static constexpr int kSlots = D == 128 ? 4 : 8;           // K/V ring depth
+  static constexpr int kSmemData = kQTiles * kTileBytes + kSlots * kTileBytes;
+  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/;
+  static constexpr uint32_t kTmemS = 0;      // S0 at col 0, S1 at col 128 (fp32)
+  static constexpr uint32_t kTmemO = 256;    // O0 at 256, O1 at 256 + D (fp32)
+};
+
+struct Barriers {
+  uint64_t q_full;
+  uint64_t s_full[kQTiles];
+  uint64_t p_full[kQTiles];
+  uint64_t o_full[kQTiles];
+  uint64_t slot_full[8];
+  uint64_t slot_empty[8];
+  uint32_t tmem_base;
+};
+
+template <int D, bool kBF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_k,
+                    const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sq = smem_u32(smem);                          // Q tiles
+  const uint32_t sring = sq + kQTiles * C::kTileBytes;         // K/V ring
+  Barriers* bars = reinterpret_cast<Barriers*>(smem + C::kSmemData);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int S = args.seq_len;
+  const int bh = blockIdx.y;
+  const int q0 = blockIdx.x * (kBM * kQTiles);
+  const int n_kv = (S + kBN - 1) / kBN;
+
+  if (threadIdx.x == 32) {
+    mbar_init(smem_u32(&bars->q_full), 1);
+    for (int t = 0; t < kQTiles; ++t) {
+      mbar_init(smem_u32(&bars->s_full[t]), 1);
+      mbar_init(smem_u32(&bars->p_full[t]), kBM);
+      mbar_init(smem_u32(&bars->o_full[t]), 1);
+    }
+    for (int s = 0; s < C::kSlots; ++s) {
+      mbar_init(smem_u32(&bars->slot_full[s]), 1);
+      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp < kSoftmaxWarp0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA
+    if (lane == 0) {
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+      const uint32_t qbar = smem_u32(&bars->q_full);
+      mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
+      for (int t = 0; t < kQTiles; ++t)
+        for (int r = 0; r < C::kRegions; ++r)
+          tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
+                      q0 + t * kBM, bh);
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n_kv; ++j) {
+        for (int kv = 0; kv < 2; ++kv) {
+          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
+          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+          mbar_arrive_expect_tx(fbar, C::kTileBytes);
+          const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
+          for (int r = 0; r < C::kRegions; ++r)
+            tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
+                        j * kBN, bh);
+          if (++slot == C::kSlots) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+      // ring position r (K_j at 2j, V_j at 2j+1) -> slot / phase
+      auto slot_of = [](int r) { return r % C::kSlots; };
+      auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
+      auto wait_full = [&](int r) {
+        mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
+        tc_fence_after();
+      };
+      auto release = [&](int r) { umma_commit(smem_u32(&bars->slot_empty[slot_of(r)])); };
+      auto issue_qk = [&](int t, int r) {
+        const uint32_t kb = sring + slot_of(r) * C::kTileBytes;
+        const uint32_t qb = sq + t * C::kTileBytes;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * C::kRegionBytes + (ks & 3) * 32;
+          umma_ss(tmem + C::kTmemS + t * kBN, sdesc_sw128(qb + off, 16, 1024),
+                  sdesc_sw128(kb + off, 16, 1024), idesc_qk, ks > 0);
+        }
+        umma_commit(smem_u32(&bars->s_full[t]));
+      };
+      auto issue_pv = [&](int t, int r, bool accumulate) {
+        const uint32_t vb = sring + slot_of(r) * C::kTileBytes;
+#pragma unroll
+        for (int ks = 0; ks < kBN / 16; ++ks) {
+          umma_ts(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
+                  sdesc_sw128(vb + ks * 16 * 128, C::kRegionBytes, 1024), idesc_pv,
+                  (accumulate || ks > 0) ? 1u : 0u);
+        }
+        umma_commit(smem_u32(&bars->o_full[t]));
+      };
+      auto wait_p = [&](int t, int j) {
+        mbar_wait(smem_u32(&bars->p_full[t]), uint32_t(j & 1));
+        tc_fence_after();
+      };
+
+      mbar_wait(smem_u32(&bars->q_full), 0);
+      tc_fence_after();
+      wait_full(0);
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      release(0);
+      for (int j = 1; j < n_kv; ++j) {
+        const int rk = 2 * j, rv = 2 * j - 1;
+        wait_full(rv);
+        wait_p(0, j - 1);
+        issue_pv(0, rv, j > 1);
+        wait_full(rk);
+        issue_qk(0, rk);
+        wait_p(1, j - 1);
+        issue_pv(1, rv, j > 1);
+        release(rv);
+        issue_qk(1, rk);
+        release(rk);
+      }
+      const int rv = 2 * n_kv - 1;
+      wait_full(rv);
+      wait_p(0, n_kv - 1);
+      issue_pv(0, rv, n_kv > 1);
+      wait_p(1, n_kv - 1);
+      issue_pv(1, rv, n_kv > 1);
+      release(rv);
+    }
+  }
+  } else {
+    // -------------------------------------------------------------- softmax
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    const int t = (warp - kSoftmaxWarp0) / 4;
+    const uint32_t wq = warp & 3;  // TMEM lane quadrant accessible to this warp
+    const int row = int(wq * 32 + lane);
+    const uint32_t lane_off = (wq * 32u) << 16;
+    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN;
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
+    const float sl2 = args.scale_log2;
+    const uint32_t sbar = smem_u32(&bars->s_full[t]);
+    const uint32_t pbar = smem_u32(&bars->p_full[t]);
+    const uint32_t obar = smem_u32(&bars->o_full[t]);
+
+    float m_run = -INFINITY;  // running max used for the exponent (scaled, log2 units)
+    float l_run = 0.f;        // running normaliser relative to m_run
+
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(sbar, uint32_t(j & 1));
+      tc_fence_after();
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
+
+      if (j == n_kv - 1) {
+        const int valid = S - j * kBN;  // keys past S were zero-filled by TMA
+        if (valid < kBN) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i >= valid) s[i] = -INFINITY;
+        }
+      }
+      // row max (8 independent chains)
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+#pragma unroll
+      for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float m_new = mx * sl2;
+      const bool need = m_new > m_run + kRescaleThreshold;
+      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
+      if (need) {
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      float sum8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
+      uint32_t pk[2][32];
+#pragma unroll
+      for (int i = 0; i < 128; i += 2) {
+        const float p0 = ex2(fmaf(s[i], sl2, -m_use));
+        const float p1 = ex2(fmaf(s[i + 1], sl2, -m_use));
+        sum8[i & 7] += p0;
+        sum8[(i + 1) & 7] += p1;
+        pk[i >> 6][(i & 63) >> 1] = pack2<kBF16>(p0, p1);
+      }
+      l_run += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) +
+               ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // O correction: wait until PV(j-1) has landed in TMEM, rescale in place
+        // (PV(j) is not issued before this warpgroup signals P(j)).
+        mbar_wait(obar, uint32_t((j - 1) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orow[32];
+          tmem_ld32(tO + c * 32, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+          tmem_st32(tO + c * 32, orow);
+        }
+      }
+      tmem_st32(tS, pk[0]);
+      tmem_st32(tS + 32, pk[1]);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(pbar);
+    }
+
+    // ------------------------------------------------------------- epilogue
+    mbar_wait(obar, uint32_t((n_kv - 1) & 1));
+    tc_fence_after();
+    const int grow = q0 + t * kBM + row;
+    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t orow[32];
+      tmem_ld32(tO + c * 32, orow);
+      tmem_wait_ld();
+      reg_fence(orow);
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
+                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
+      if (grow < S) {
+        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                              packed[4 * i + 3]);
+      }
+    }
+    if (args.lse != nullptr && grow < S)
+      args.lse[size_t(bh) * S + grow] =
+          l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
+}
+
+// ----------------------------------------------------------------------------
+// Descriptor self-test: one 128x128x128 UMMA product, checked on the host.
+//   mode 0: D = A * B^T, A [128][128] K-major, B [128 n][128 k] K-major (QK^T)
+//   mode 1: D = A * B,   A K-major, B [128 k][128 n] MN-major       (PV, SS)
+//   mode 2: as mode 1 but A staged in TMEM via tcgen05.st (TS-MMA)  (PV, TS)
+// ----------------------------------------------------------------------------
+template <bool kBF16>
+__global__ void __launch_bounds__(128, 1)
+    umma_selftest_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                         const __grid_constant__ CUtensorMap tmap_b, const uint16_t* a_glob,
+                         float* d_out, int mode) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sa = smem_u32(smem);
+  const uint32_t sb = sa + 32768;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 65536 + 64);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar[0]), 1);
+    mbar_init(smem_u32(&bar[1]), 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(smem_u32(tmem_holder));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(smem_u32(&bar[0]), 65536);
+    for (int r = 0; r < 2; ++r) {
+      tma_load_3d(sa + r * 16384, &tmap_a, smem_u32(&bar[0]), r * 64, 0, 0);
+      tma_load_3d(sb + r * 16384, &tmap_b, smem_u32(&bar[0]), r * 64, 0, 0);
+    }
+  }
+  if (mode == 2) {
+    // row = thread; A row (128 x 16-bit = 64 x b32) into TMEM cols 128..191
+    const int row = int(threadIdx.x);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a_glob + size_t(row) * 128);
+    uint32_t r0[32], r1[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      r0[i] = src[i];
+      r1[i] = src[32 + i];
+    }
+    const uint32_t base = tmem + ((warp * 32u) << 16) + 128;
+    tmem_st32(base, r0);
+    tmem_st32(base + 32, r1);
+    tmem_wait_st();
+  }
+  mbar_wait(smem_u32(&bar[0]), 0);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_f16(kBF16, 128, 128, false, mode != 0);
+    for (int ks = 0; ks < 8; ++ks) {
+      const uint32_t koff = (ks >> 2) * 16384 + (ks & 3) * 32;
+      const uint64_t adesc = sdesc_sw128(sa + koff, 16, 1024);
+      if (mode == 0) {
+        umma_ss(tmem, adesc, sdesc_sw128(sb + koff, 16, 1024), idesc, ks > 0);
+      } else if (mode == 1) {
+        umma_ss(tmem, adesc, sdesc_sw128(sb + ks * 2048, 16384, 1024), idesc, ks > 0);
+      } else {
+        umma_ts(tmem, tmem + 128 + ks * 8, sdesc_sw128(sb + ks * 2048, 16384, 1024), idesc,
+                ks > 0);
+      }
+    }
+    umma_commit(smem_u32(&bar[1]));
+  }
+  mbar_wait(smem_u32(&bar[1]), 0);
+  tc_fence_after();
+  const int row = int(warp * 32 + lane);
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[32];
+    tmem_ld32(tmem + ((warp * 32u) << 16) + c * 32, r);
+    tmem_wait_ld();
+    reg_fence(r);
+    for (int i = 0; i < 32; ++i) d_out[size_t(row) * 128 + c * 32 + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+template <int D, bool kBF16>
+cudaError_t launch_typed(const FwdLaunch& L) {
+  using C = Cfg<D>;
+  auto kern = sdpa_fwd_kernel<D, kBF16>;
+  static bool attr_set[64] = {};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  const int rows_per_cta = kBM * kQTiles;
+  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
+  kern<<<grid, kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+FwdGeometry fwd_geometry(int64_t S, int64_t BH) {
+  FwdGeometry g;
+  g.block_m = kBM;
+  g.block_n = kBN;
+  g.q_tiles_per_cta = kQTiles;
+  g.threads = kThreads;
+  g.ctas = ((S + kBM * kQTiles - 1) / (kBM * kQTiles)) * BH;
+  return g;
+}
+
+int fwd_ring_slots(int D) { return D == 128 ? Cfg<128>::kSlots : Cfg<64>::kSlots; }
+
+cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
+  if (L.head_dim == 128) return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
+  if (L.head_dim == 64) return L.bf16 ? launch_typed<64, true>(L) : launch_typed<64, false>(L);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_umma_selftest(const CUtensorMap* ta_map, const CUtensorMap* tb_map,
+                                 const void* a_glob, float* d_out, int mode, bool bf16,
+                                 void* stream) {
+  const int smem = 65536 + 1024 + 1024;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (bf16) {
+    cudaFuncSetAttribute(umma_selftest_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    umma_selftest_kernel<true><<<1, 128, smem, st>>>(
+        *ta_map, *tb_map, static_cast<const uint16_t*>(a_glob), d_out, mode);
+  } else {
+    cudaFuncSetAttribute(umma_selftest_kernel<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    umma_selftest_kernel<false><<<1, 128, smem, st>>>(
+        *ta_map, *tb_map, static_cast<const uint16_t*>(a_glob), d_out, mode);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ta

@@ -1,0 +1,45 @@
+// Internal interface between the C-ABI host layer (c_api.cpp) and the
+// sm_100a kernels (sdpa_fwd_sm100.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ta {
+
+struct FwdArgs {
+  void* o;           // [BH, S, D] 16-bit, same dtype as inputs
+  float* lse;        // [BH, S] fp32 natural-log LSE, or nullptr
+  int seq_len;       // S
+  float scale_log2;  // softmax scale * log2(e)
+};
+
+struct FwdLaunch {
+  const CUtensorMap* tmap_q;
+  const CUtensorMap* tmap_k;
+  const CUtensorMap* tmap_v;
+  FwdArgs args;
+  int64_t bh;
+  int head_dim;
+  bool bf16;
+  void* stream;
+};
+
+struct FwdGeometry {
+  int block_m;
+  int block_n;
+  int q_tiles_per_cta;
+  int threads;
+  int64_t ctas;
+};
+
+FwdGeometry fwd_geometry(int64_t S, int64_t BH);
+int fwd_ring_slots(int D);
+cudaError_t launch_sdpa_fwd(const FwdLaunch& launch);
+cudaError_t launch_umma_selftest(const CUtensorMap* a_map, const CUtensorMap* b_map,
+                                 const void* a_glob, float* d_out, int mode, bool bf16,
+                                 void* stream);
+
+}  // namespace ta

@@ -1,0 +1,201 @@
+"""GPU parity: the sm_100a kernel (through the C-ABI) against the CPU oracle.
+
+Tolerances (max-abs on O, unit-variance inputs):
+  reference gate (bench.cpp:56-63):   f16 5e-3, bf16 2e-2
+  BASELINE.json north_star:           f16 1e-2, bf16 2e-2
+  LSE (new output):                   1e-3 absolute
+The kernel quantises P to 16 bits before the PV MMA (as every tensor-core
+attention does); the fp32 statistics keep the error well inside the gate.
+"""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+META = json.loads((GOLD / "golden.json").read_text())
+TOL = {O.F16: 5e-3, O.BF16: 2e-2}
+LSE_TOL = 1e-3
+
+
+def _tdt(dt):
+    import torch
+    return {O.F16: torch.float16, O.BF16: torch.bfloat16}[dt]
+
+
+def run_gpu(ta, q, k, v, dt, scale=None, stats=None, causal=False):
+    import torch
+    qd, kd, vd = (torch.from_numpy(np.ascontiguousarray(x)).to(_tdt(dt)).cuda() for x in (q, k, v))
+    o, lse = ta.sdpa(qd, kd, vd, causal=causal, scale=scale, return_lse=True, stats=stats)
+    torch.cuda.synchronize()
+    return o.double().cpu().numpy(), lse.double().cpu().numpy()
+
+
+# ------------------------------------------------------------------ UMMA unit
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("dt", [O.BF16, O.F16])
+def test_umma_descriptor_selftest(ta, cuda_device, mode, dt):
+    import torch
+    g = torch.Generator().manual_seed(mode * 10 + dt)
+    a = torch.randn(128, 128, generator=g).to(_tdt(dt)).cuda()
+    b = torch.randn(128, 128, generator=g).to(_tdt(dt)).cuda()
+    d = torch.empty(128, 128, dtype=torch.float32, device="cuda")
+    rc = ta.lib().ta_debug_umma_gemm(mode, dt, a.data_ptr(), b.data_ptr(), d.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream)
+    ta._check(rc)
+    want = a.double() @ (b.double().T if mode == 0 else b.double())
+    err = (d.double() - want).abs().max().item()
+    assert err <= 1e-3, f"mode {mode}: max err {err}"
+
+
+# ---------------------------------------------------------- golden fixtures
+@pytest.mark.parametrize("name", sorted(META["cases"]))
+def test_kernel_matches_reference_golden(ta, cuda_device, name):
+    c = META["cases"][name]
+    B, H, S, D = c["shape"]
+    dt = c["dtype"]
+    g = np.load(GOLD / f"{name}.npz")
+    q, k, v = O.make_input((B, H, S, D), dt, c["seed"])
+    o, lse = run_gpu(ta, q, k, v, dt)
+    keep = c["heads_kept"]
+    err_o = np.abs(o.reshape(B * H, S, D)[:keep] - g["o"]).max()
+    err_l = np.abs(lse.reshape(B * H, S) - g["lse"]).max()
+    assert err_o <= TOL[dt], err_o
+    assert err_l <= LSE_TOL, err_l
+
+
+# ------------------------------------------------------ oracle, full tensors
+@pytest.mark.parametrize("dt", [O.F16, O.BF16])
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("S", [1, 17, 128, 130, 256, 300, 512, 640])
+def test_kernel_matches_oracle(ta, cuda_device, dt, D, S):
+    B, H = 1, 3
+    q, k, v = O.make_input((B, H, S, D), dt, 1000 + S)
+    o, lse = run_gpu(ta, q, k, v, dt)
+    r = O.sdpa_reference(q, k, v)
+    assert np.abs(o - r["o"]).max() <= TOL[dt]
+    assert np.abs(lse - r["lse"]).max() <= LSE_TOL
+
+
+def test_cfg1_full_parity(ta, cuda_device):
+    # BASELINE configs[0]: B=1 H=8 S=512 D=64 FP16 non-causal, all heads
+    q, k, v = O.make_input((1, 8, 512, 64), O.F16, 0)
+    o, lse = run_gpu(ta, q, k, v, O.F16)
+    r = O.sdpa_reference(q, k, v)
+    err = np.abs(o - r["o"]).max()
+    assert err <= 5e-3, err
+    assert np.abs(lse - r["lse"]).max() <= LSE_TOL
+
+
+def test_output_on_dtype_grid_and_matches_snapped_oracle(ta, cuda_device):
+    # finalize + snap (tiled.cpp:216-220): the kernel's output is 16-bit, i.e.
+    # on the grid; compare with the oracle snapped to the same grid
+    q, k, v = O.make_input((1, 2, 256, 64), O.BF16, 5)
+    o, _ = run_gpu(ta, q, k, v, O.BF16)
+    snapped = np.vectorize(lambda x: O.snap(float(x), O.BF16))(o.ravel()[:2048])
+    assert np.array_equal(snapped, o.ravel()[:2048])
+
+
+@pytest.mark.parametrize("scale", [0.5, 0.02])
+def test_explicit_scale(ta, cuda_device, scale):
+    q, k, v = O.make_input((1, 2, 384, 128), O.BF16, 9)
+    o, lse = run_gpu(ta, q, k, v, O.BF16, scale=scale)
+    r = O.sdpa_reference(q, k, v, scale=scale)
+    assert np.abs(o - r["o"]).max() <= TOL[O.BF16]
+    assert np.abs(lse - r["lse"]).max() <= LSE_TOL
+
+
+def test_large_scores_exercise_lazy_rescale(ta, cuda_device):
+    # scale 1.0 on D=128 N(0,1) inputs gives score std ~11: the running max
+    # grows by more than 2^8 across tiles, so the O correction path runs.
+    q, k, v = O.make_input((1, 2, 1024, 128), O.F16, 21)
+    o, lse = run_gpu(ta, q, k, v, O.F16, scale=1.0)
+    r = O.sdpa_reference(q, k, v, scale=1.0)
+    assert np.abs(o - r["o"]).max() <= 1e-2
+    assert np.abs(lse - r["lse"]).max() <= LSE_TOL * 10  # |LSE| ~ 40 here
+
+
+# ------------------------------------------------- larger S, sampled heads
+@pytest.mark.parametrize("D,dt", [(64, O.BF16), (128, O.BF16), (128, O.F16)])
+def test_long_sequence_sampled_heads(ta, cuda_device, D, dt):
+    B, H, S = 1, 4, 4096
+    q, k, v = O.make_input((B, H, S, D), dt, 77)
+    o, lse = run_gpu(ta, q, k, v, dt)
+    for h in (0, 3):
+        on, ln = O.sdpa_numpy(q[0, h], k[0, h], v[0, h])
+        assert np.abs(o[0, h] - on).max() <= TOL[dt]
+        assert np.abs(lse[0, h] - ln).max() <= LSE_TOL
+
+
+# --------------------------------------------- size-independent properties
+def test_zero_queries_give_mean_of_values(ta, cuda_device):
+    # test_reference.cpp:91-103 at a large size: O = mean(V), LSE = ln S
+    import torch
+    B, H, S, D = 2, 4, 8192, 128
+    k = torch.randn(B, H, S, D, device="cuda").bfloat16()
+    v = torch.randn(B, H, S, D, device="cuda").bfloat16()
+    q = torch.zeros_like(k)
+    o, lse = ta.sdpa(q, k, v, return_lse=True)
+    mean = v.double().mean(dim=2, keepdim=True).expand_as(o)
+    assert (o.double() - mean).abs().max().item() <= 2e-3
+    assert (lse.double() - math.log(S)).abs().max().item() <= 1e-4
+
+
+def test_key_permutation_equivariance(ta, cuda_device):
+    # test_reference.cpp:130-146: permuting K/V rows together leaves O unchanged
+    import torch
+    B, H, S, D = 1, 4, 2048, 128
+    q = torch.randn(B, H, S, D, device="cuda").bfloat16()
+    k = torch.randn(B, H, S, D, device="cuda").bfloat16()
+    v = torch.randn(B, H, S, D, device="cuda").bfloat16()
+    perm = torch.randperm(S, device="cuda")
+    o1, l1 = ta.sdpa(q, k, v, return_lse=True)
+    o2, l2 = ta.sdpa(q, k[:, :, perm], v[:, :, perm], return_lse=True)
+    assert (o1.float() - o2.float()).abs().max().item() <= 2e-2
+    assert (l1 - l2).abs().max().item() <= 1e-4
+
+
+def test_bitwise_deterministic(ta, cuda_device):
+    # test_tiled.cpp:387-400 analogue: no atomics, disjoint rows per CTA
+    import torch
+    q, k, v = (torch.randn(2, 8, 3000, 64, device="cuda").half() for _ in range(3))
+    a = ta.sdpa(q, k, v)
+    b = ta.sdpa(q, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_host_entry_matches_device_entry(ta, cuda_device):
+    import torch
+    q, k, v = O.make_input((1, 2, 700, 128), O.BF16, 4)
+    got = ta.sdpa_tiled(q, k, v, dtype=ta.BF16)
+    o, _ = run_gpu(ta, q, k, v, O.BF16)
+    assert np.array_equal(got.astype(np.float64), o)
+    r = O.sdpa_reference(q, k, v)
+    assert np.abs(got - r["o"]).max() <= TOL[O.BF16]
+
+
+def test_stats_report_executed_tiling(ta, cuda_device):
+    st = ta.KernelStats()
+    q, k, v = O.make_input((1, 2, 1000, 64), O.F16, 1)
+    run_gpu(ta, q, k, v, O.F16, stats=st)
+    assert st.block_m == 128 and st.block_n == 128
+    # one (bh, 128-row tile) item streams ceil(S/128) K/V tiles
+    assert st.kv_tiles_visited == 2 * 8 * 8
+    assert st.ctas == 2 * 4
+
+
+def test_errors_are_loud(ta, cuda_device):
+    import torch
+    x = torch.zeros(1, 1, 64, 48, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(ta.UnsupportedScheduleError):
+        ta.sdpa(x, x, x)
+    y = torch.zeros(1, 1, 64, 64, device="cuda", dtype=torch.float32)
+    with pytest.raises(ta.UnsupportedScheduleError):
+        ta.sdpa(y, y, y)
