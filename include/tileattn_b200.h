@@ -142,6 +142,13 @@ TA_API int ta_device_supported(int device);
 TA_API ta_status ta_debug_umma_gemm(int mode, ta_dtype dtype, const void* a, const void* b, float* d,
                              void* stream);
 
+/* Diagnostics: run the forward once with a cycle-timeline trace of CTA (0,0):
+ * trace (device, int64[14 * 64]) receives clock64 stamps per event and K/V
+ * iteration (event ids: see TraceEvent in csrc/sdpa_fwd_sm100.h).  Synchronous. */
+TA_API ta_status ta_debug_sdpa_trace(const void* q, const void* k, const void* v, void* o,
+                                     ta_shape shape, ta_dtype dtype, long long* trace,
+                                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

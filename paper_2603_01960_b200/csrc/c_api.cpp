@@ -219,7 +219,8 @@ void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh) {
 }
 
 ta_status run_device(const void* q, const void* k, const void* v, void* o, float* lse,
-                     ta_shape sh, ta_dtype dt, double scale, const Plan& plan, void* stream) {
+                     ta_shape sh, ta_dtype dt, double scale, const Plan& plan, void* stream,
+                     long long* trace = nullptr) {
   const bool bf16 = dt == TA_BF16;
   const int64_t bh = sh.b * sh.h;
   CUtensorMap mq, mk, mv;
@@ -235,6 +236,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.args.lse = lse;
   L.args.seq_len = int(sh.s);
   L.args.scale_log2 = float(scale * 1.4426950408889634074);
+  L.args.trace = trace;
   L.bh = bh;
   L.head_dim = int(sh.d);
   L.bf16 = bf16;
@@ -370,6 +372,22 @@ ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o,
     return cuda_fail(e, "D2H copy");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
   fill_stats(stats, *plan, shape);
+  return TA_OK;
+}
+
+ta_status ta_debug_sdpa_trace(const void* q, const void* k, const void* v, void* o,
+                              ta_shape shape, ta_dtype dtype, long long* trace, void* stream) {
+  double eff = 0.0;
+  ta_schedule sched = resolve_schedule(ta_schedule{0, 0, 0, 0});
+  ta_status st = validate_common(shape, TA_MASK_NONE, nullptr, sched, 0, 0.0, &eff);
+  if (st != TA_OK) return st;
+  if ((st = validate_device_support(shape, dtype, TA_MASK_NONE)) != TA_OK) return st;
+  if ((st = check_device()) != TA_OK) return st;
+  auto plan = get_plan(sched, shape.d, dtype, false);
+  if ((st = run_device(q, k, v, o, nullptr, shape, dtype, eff, *plan, stream, trace)) != TA_OK)
+    return st;
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "trace sync");
   return TA_OK;
 }
 

@@ -83,6 +83,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int bh = blockIdx.y;
   const int q0 = blockIdx.x * (kBM * kQTiles);
   const int n_kv = (S + kBN - 1) / kBN;
+  long long* const trace =
+      (args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+  auto rec = [&](int ev, int j) {
+    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
+  };
 
   if (threadIdx.x == 32) {
     mbar_init(smem_u32(&bars->q_full), 1);
@@ -184,14 +189,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rk = 2 * j, rv = 2 * j - 1;
         wait_full(rv);
         wait_p(0, j - 1);
+        rec(kEvMmaWaitP0, j);
         issue_pv(0, rv, j > 1);
         wait_full(rk);
         issue_qk(0, rk);
+        rec(kEvMmaIssuedPV0, j);
         wait_p(1, j - 1);
+        rec(kEvMmaWaitP1, j);
         issue_pv(1, rv, j > 1);
         release(rv);
         issue_qk(1, rk);
         release(rk);
+        rec(kEvMmaIssuedPV1, j);
       }
       const int rv = 2 * n_kv - 1;
       wait_full(rv);
@@ -222,12 +231,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(sbar, uint32_t(j & 1));
       tc_fence_after();
+      const bool tr = (row == 0);
+      if (tr) rec(kEvSm0SReady + 5 * t, j);
       uint32_t sr[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
       tmem_wait_ld();
 #pragma unroll
       for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
+      if (tr) rec(kEvSm0Loaded + 5 * t, j);
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -251,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float m_new = mx * sl2;
+      if (tr) rec(kEvSm0Max + 5 * t, j);
       const bool need = m_new > m_run + kRescaleThreshold;
       const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
       if (need) {
@@ -272,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       l_run += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) +
                ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+      if (tr) rec(kEvSm0Exp + 5 * t, j);
       if (j > 0 && __any_sync(0xffffffffu, need)) {
         // O correction: wait until PV(j-1) has landed in TMEM, rescale in place
         // (PV(j) is not issued before this warpgroup signals P(j)).
@@ -294,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(pbar);
+      if (tr) rec(kEvSm0PArrive + 5 * t, j);
     }
 
     // ------------------------------------------------------------- epilogue

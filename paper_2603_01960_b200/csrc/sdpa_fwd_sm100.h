@@ -14,6 +14,29 @@ struct FwdArgs {
   float* lse;        // [BH, S] fp32 natural-log LSE, or nullptr
   int seq_len;       // S
   float scale_log2;  // softmax scale * log2(e)
+  // diagnostics: when non-null, CTA (0,0) records clock64 timestamps
+  // trace[event * kTraceIters + j] for the first kTraceIters K/V iterations
+  long long* trace;
+};
+
+constexpr int kTraceIters = 64;
+// trace events
+enum TraceEvent {
+  kEvMmaWaitP0 = 0,  // MMA warp: P0(j-1) ready observed
+  kEvMmaIssuedPV0,   // PV0(j-1) + S0(j) issued
+  kEvMmaWaitP1,      // P1(j-1) ready observed
+  kEvMmaIssuedPV1,   // PV1(j-1) + S1(j) issued
+  kEvSm0SReady,      // softmax WG0: S0(j) observed ready
+  kEvSm0Loaded,      // S0 in registers
+  kEvSm0Max,         // row max done
+  kEvSm0Exp,         // exps + pack done
+  kEvSm0PArrive,     // P0(j) written + arrived
+  kEvSm1SReady,
+  kEvSm1Loaded,
+  kEvSm1Max,
+  kEvSm1Exp,
+  kEvSm1PArrive,
+  kNumTraceEvents
 };
 
 struct FwdLaunch {
