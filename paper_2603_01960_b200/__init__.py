@@ -30,7 +30,11 @@ __all__ = [
 ]
 
 _PKG = Path(__file__).resolve().parent
-_LIB_PATH = _PKG / "_lib" / "libtileattn_b200.so"
+import os as _os
+
+# TILEATTN_B200_LIB: load an alternative build of the same C-ABI (tuning
+# experiments); the default is the in-tree library.
+_LIB_PATH = Path(_os.environ.get("TILEATTN_B200_LIB", _PKG / "_lib" / "libtileattn_b200.so"))
 
 TA_OK, TA_ERR_INVALID_ARGUMENT, TA_ERR_UNSUPPORTED, TA_ERR_OOM, TA_ERR_CUDA = range(5)
 F32, F16, BF16 = 0, 1, 2

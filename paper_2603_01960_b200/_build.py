@@ -17,7 +17,6 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libtileattn_b200.so"
-STAMP = LIBDIR / "libtileattn_b200.stamp"
 
 SOURCES = [CSRC / "sdpa_fwd_sm100.cu", CSRC / "c_api.cpp"]
 HEADERS = [CSRC / "ptx_sm100.cuh", CSRC / "sdpa_fwd_sm100.h", ROOT / "include" / "tileattn_b200.h"]
@@ -51,30 +50,39 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile (if sources changed) and return the library path."""
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Compile (if sources changed) and return the library path.
+
+    ``defines``/``out`` build an experimental variant (e.g. -DTA_EMU_PER8=3)
+    into another file; the product library is the default ``LIB``."""
     LIBDIR.mkdir(exist_ok=True)
-    dig = _digest()
-    if not force and LIB.exists() and STAMP.exists() and STAMP.read_text() == dig:
-        return LIB
-    objdir = LIBDIR / "obj"
+    lib = Path(out) if out else LIB
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    stamp = lib.with_suffix(".stamp")
+    dig = _digest() + "|".join(defines)
+    if not force and lib.exists() and stamp.exists() and stamp.read_text() == dig:
+        return lib
+    objdir = LIBDIR / ("obj" if out is None else "obj_" + lib.stem)
     objdir.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = objdir / (src.stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     subprocess.run([nvcc(), GENCODE, "-shared", "-o", str(tmp), *objs, "-cudart", "static"],
                    check=True)
-    os.replace(tmp, LIB)
-    STAMP.write_text(dig)
-    return LIB
+    os.replace(tmp, lib)
+    stamp.write_text(dig)
+    return lib
 
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                out=Path(outs[0]) if outs else None))

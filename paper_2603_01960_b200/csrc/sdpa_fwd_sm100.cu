@@ -35,12 +35,18 @@ constexpr int kThreads = 384;   // 12 warps
 constexpr int kSoftmaxWarp0 = 4;  // warps 4..7 -> Q tile 0, 8..11 -> Q tile 1
 constexpr uint32_t kTmemCols = 512;
 // register split: 4 control warps (TMA, MMA, TMEM alloc, spare) + 8 softmax warps
-constexpr int kRegsControl = 96;
-constexpr int kRegsSoftmax = 200;  // 128*96 + 256*200 <= 64K
+constexpr int kRegsControl = 88;
+constexpr int kRegsSoftmax = 208;  // 128*88 + 256*208 <= 64K
 constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
 constexpr float kRescaleThreshold = 8.0f;
+// exp2 work split: of every 8 score columns, kEmuPer8 use the FMA-pipe
+// polynomial (ex2_poly) and the rest the MUFU (measured 16 exp2/clk/SM).
+#ifndef TA_EMU_PER8
+#define TA_EMU_PER8 2
+#endif
+constexpr int kEmuPer8 = TA_EMU_PER8;
 
 template <int D>
 struct Cfg {
@@ -57,7 +63,7 @@ struct Cfg {
 struct Barriers {
   uint64_t q_full;
   uint64_t s_full[kQTiles];
-  uint64_t p_full[kQTiles];
+  uint64_t p_full[kQTiles][2];  // P columns [0,64) / [64,128) written
   uint64_t o_full[kQTiles];
   uint64_t slot_full[8];
   uint64_t slot_empty[8];
@@ -93,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&bars->q_full), 1);
     for (int t = 0; t < kQTiles; ++t) {
       mbar_init(smem_u32(&bars->s_full[t]), 1);
-      mbar_init(smem_u32(&bars->p_full[t]), kBM);
+      mbar_init(smem_u32(&bars->p_full[t][0]), kBM / 32);  // one arrive per warp
+      mbar_init(smem_u32(&bars->p_full[t][1]), kBM / 32);
       mbar_init(smem_u32(&bars->o_full[t]), 1);
     }
     for (int s = 0; s < C::kSlots; ++s) {
@@ -153,30 +160,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
       };
       auto release = [&](int r) { umma_commit(smem_u32(&bars->slot_empty[slot_of(r)])); };
+      // descriptors: base built once, K-step offsets added to the start-address
+      // field (addr >> 4; smem addresses < 256 KB never carry out of 14 bits)
+      const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
+      const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
+      const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
       auto issue_qk = [&](int t, int r) {
-        const uint32_t kb = sring + slot_of(r) * C::kTileBytes;
-        const uint32_t qb = sq + t * C::kTileBytes;
+        uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
+        uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+        // opaque to the optimiser: stops 2 x 8 per-K-step descriptors being
+        // hoisted out of the K/V loop into (spilled) registers
+        asm volatile("" : "+l"(qd), "+l"(kd));
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * C::kRegionBytes + (ks & 3) * 32;
-          umma_ss(tmem + C::kTmemS + t * kBN, sdesc_sw128(qb + off, 16, 1024),
-                  sdesc_sw128(kb + off, 16, 1024), idesc_qk, ks > 0);
+          const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
+          umma_ss(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
         }
         umma_commit(smem_u32(&bars->s_full[t]));
       };
-      auto issue_pv = [&](int t, int r, bool accumulate) {
-        const uint32_t vb = sring + slot_of(r) * C::kTileBytes;
+      // PV in two halves of 64 keys, each issued as soon as the softmax
+      // warpgroup has written that half of P (P aliases S in TMEM).
+      auto issue_pv = [&](int t, int r, bool accumulate, int j) {
+        uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+        asm volatile("" : "+l"(vd));
 #pragma unroll
-        for (int ks = 0; ks < kBN / 16; ++ks) {
-          umma_ts(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
-                  sdesc_sw128(vb + ks * 16 * 128, C::kRegionBytes, 1024), idesc_pv,
-                  (accumulate || ks > 0) ? 1u : 0u);
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(smem_u32(&bars->p_full[t][h]), uint32_t(j & 1));
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kBN / 32; ++kk) {
+            const int ks = h * (kBN / 32) + kk;
+            umma_ts(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
+                    vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+                    (accumulate || ks > 0) ? 1u : 0u);
+          }
         }
         umma_commit(smem_u32(&bars->o_full[t]));
-      };
-      auto wait_p = [&](int t, int j) {
-        mbar_wait(smem_u32(&bars->p_full[t]), uint32_t(j & 1));
-        tc_fence_after();
       };
 
       mbar_wait(smem_u32(&bars->q_full), 0);
@@ -188,15 +207,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 1; j < n_kv; ++j) {
         const int rk = 2 * j, rv = 2 * j - 1;
         wait_full(rv);
-        wait_p(0, j - 1);
         rec(kEvMmaWaitP0, j);
-        issue_pv(0, rv, j > 1);
+        issue_pv(0, rv, j > 1, j - 1);
         wait_full(rk);
         issue_qk(0, rk);
         rec(kEvMmaIssuedPV0, j);
-        wait_p(1, j - 1);
         rec(kEvMmaWaitP1, j);
-        issue_pv(1, rv, j > 1);
+        issue_pv(1, rv, j > 1, j - 1);
         release(rv);
         issue_qk(1, rk);
         release(rk);
@@ -204,10 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int rv = 2 * n_kv - 1;
       wait_full(rv);
-      wait_p(0, n_kv - 1);
-      issue_pv(0, rv, n_kv > 1);
-      wait_p(1, n_kv - 1);
-      issue_pv(1, rv, n_kv > 1);
+      issue_pv(0, rv, n_kv > 1, n_kv - 1);
+      issue_pv(1, rv, n_kv > 1, n_kv - 1);
       release(rv);
     }
   }
@@ -222,7 +237,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
     const float sl2 = args.scale_log2;
     const uint32_t sbar = smem_u32(&bars->s_full[t]);
-    const uint32_t pbar = smem_u32(&bars->p_full[t]);
     const uint32_t obar = smem_u32(&bars->o_full[t]);
 
     float m_run = -INFINITY;  // running max used for the exponent (scaled, log2 units)
@@ -270,25 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run *= alpha;
         m_run = m_new;
       }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      float sum8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
-      uint32_t pk[2][32];
-#pragma unroll
-      for (int i = 0; i < 128; i += 2) {
-        const float p0 = ex2(fmaf(s[i], sl2, -m_use));
-        const float p1 = ex2(fmaf(s[i + 1], sl2, -m_use));
-        sum8[i & 7] += p0;
-        sum8[(i + 1) & 7] += p1;
-        pk[i >> 6][(i & 63) >> 1] = pack2<kBF16>(p0, p1);
-      }
-      l_run += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) +
-               ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
-      if (tr) rec(kEvSm0Exp + 5 * t, j);
       if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // O correction: wait until PV(j-1) has landed in TMEM, rescale in place
-        // (PV(j) is not issued before this warpgroup signals P(j)).
+        // O correction (rare with the lazy threshold): wait until PV(j-1) has
+        // landed in TMEM and rescale in place; PV(j) is not issued before this
+        // warpgroup signals the first half of P(j).
         mbar_wait(obar, uint32_t((j - 1) & 1));
         tc_fence_after();
 #pragma unroll
@@ -303,11 +302,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(tO + c * 32, orow);
         }
       }
-      tmem_st32(tS, pk[0]);
-      tmem_st32(tS + 32, pk[1]);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(pbar);
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      float sum8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          const int c = h * 64 + i;
+          const float x0 = fmaf(s[c], sl2, -m_use);
+          const float x1 = fmaf(s[c + 1], sl2, -m_use);
+          // split the exp2 work between the MUFU and the FMA pipe
+          const float p0 = ((c & 7) < kEmuPer8) ? ex2_poly(x0) : ex2(x0);
+          const float p1 = (((c + 1) & 7) < kEmuPer8) ? ex2_poly(x1) : ex2(x1);
+          sum8[c & 7] += p0;
+          sum8[(c + 1) & 7] += p1;
+          pk[i >> 1] = pack2<kBF16>(p0, p1);
+        }
+        tmem_st32(tS + h * 32, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
+        if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
+      }
+      l_run += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) +
+               ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
       if (tr) rec(kEvSm0PArrive + 5 * t, j);
     }
 
