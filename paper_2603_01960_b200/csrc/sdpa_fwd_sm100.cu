@@ -303,23 +303,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      float sum8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) sum8[i] = 0.f;
+      // x = s * scale*log2e - m as packed FFMA2; exp2 split between the MUFU
+      // and the FMA pipe (kEmuPer8 of every 8 columns, emulated in pairs);
+      // row sum as packed FADD2 into 4 pair accumulators.
+      const uint64_t sl2x2 = f2(sl2, sl2);
+      const uint64_t negm2 = f2(-m_use, -m_use);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          const int c = h * 64 + i;
-          const float x0 = fmaf(s[c], sl2, -m_use);
-          const float x1 = fmaf(s[c + 1], sl2, -m_use);
-          // split the exp2 work between the MUFU and the FMA pipe
-          const float p0 = ((c & 7) < kEmuPer8) ? ex2_poly(x0) : ex2(x0);
-          const float p1 = (((c + 1) & 7) < kEmuPer8) ? ex2_poly(x1) : ex2(x1);
-          sum8[c & 7] += p0;
-          sum8[(c + 1) & 7] += p1;
-          pk[i >> 1] = pack2<kBF16>(p0, p1);
+        for (int g = 0; g < 8; ++g) {  // groups of 8 columns
+          const int c0 = h * 64 + g * 8;
+          uint64_t x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
+          float p[8];
+          // emulated pairs are the last kEmuPer8/2 pairs of the group
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (2 * u >= 8 - kEmuPer8) {
+              ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
+            } else {
+              float a, b;
+              f2_split(x[u], a, b);
+              p[2 * u] = ex2(a);
+              p[2 * u + 1] = ex2(b);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
+            pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+          }
         }
         tmem_st32(tS + h * 32, pk);
         tmem_wait_st();
@@ -328,8 +345,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
         if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
       }
-      l_run += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) +
-               ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+      {
+        const uint64_t a01 = fadd2(acc[0], acc[1]);
+        const uint64_t a23 = fadd2(acc[2], acc[3]);
+        float lo, hi;
+        f2_split(fadd2(a01, a23), lo, hi);
+        l_run += lo + hi;
+      }
       if (tr) rec(kEvSm0PArrive + 5 * t, j);
     }
 
