@@ -36,9 +36,9 @@ constexpr int kThreads = 384;   // 12 warps
 // eligible warps, so the latency-critical single-thread roles (MMA issue, TMA)
 // take the top ids and are never starved by the softmax warps' issue stream.
 constexpr int kNumSoftmaxWarps = 8;  // warps 0..3 -> Q tile 0, 4..7 -> Q tile 1
-constexpr int kWarpAlloc = 8;        // TMEM allocator (+ optional tracer)
+constexpr int kWarpAlloc = 8;        // TMEM allocator (otherwise idle)
 constexpr int kWarpTma = 9;
-constexpr int kWarpMma0 = 10;        // MMA issuer for Q tile 0; 11 for Q tile 1
+constexpr int kWarpMma = 11;
 constexpr uint32_t kTmemCols = 512;
 // register split: 4 control warps (TMA, MMA, TMEM alloc, spare) + 8 softmax warps
 constexpr int kRegsControl = 88;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
   };
 
-  if (threadIdx.x == kWarpTma * 32) {
+  if (threadIdx.x == kWarpMma * 32) {
     mbar_init(smem_u32(&bars->q_full), 1);
     for (int t = 0; t < kQTiles; ++t) {
       mbar_init(smem_u32(&bars->s_full[t]), 1);
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < C::kSlots; ++s) {
       mbar_init(smem_u32(&bars->slot_full[s]), 1);
-      mbar_init(smem_u32(&bars->slot_empty[s]), kQTiles);  // one commit per MMA stream
+      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
     }
     fence_barrier_init();
   }
@@ -153,31 +153,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kWarpAlloc) {
-    // optional tracer: timestamps of tensor-core completions (diagnostics only)
-    if (lane == 0 && trace != nullptr) {
-      for (int j = 0; j < n_kv && j < kTraceIters; ++j) {
-        mbar_wait(smem_u32(&bars->o_full[0]), uint32_t(j & 1));
-        rec(kEvTcPV0Done, j);
-        if (j + 1 < n_kv) {
-          mbar_wait(smem_u32(&bars->s_full[0]), uint32_t((j + 1) & 1));
-          rec(kEvTcS0Done, j);
-        }
-        mbar_wait(smem_u32(&bars->o_full[1]), uint32_t(j & 1));
-        rec(kEvTcPV1Done, j);
-        if (j + 1 < n_kv) {
-          mbar_wait(smem_u32(&bars->s_full[1]), uint32_t((j + 1) & 1));
-          rec(kEvTcS1Done, j);
-        }
-      }
-    }
-  } else if (warp >= kWarpMma0) {
+  } else if (warp == kWarpMma) {
     // ------------------------------------------------------------------ MMA
-    // One issuing thread per Q tile: each stream's barrier waits are covered
-    // by the other stream's MMAs (the tensor core queue is only a few MMAs
-    // deep).  Within a stream, PV_t(j-1) precedes S_t(j) (P_t aliases S_t).
     if (lane == 0) {
-      const int t = int(warp) - kWarpMma0;
       constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
       constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
       // ring position r (K_j at 2j, V_j at 2j+1) -> slot / phase
@@ -187,31 +165,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
         tc_fence_after();
       };
-      // the slot is free once both streams' MMAs reading it have completed
       auto release = [&](int r) { umma_commit(smem_u32(&bars->slot_empty[slot_of(r)])); };
       // descriptors: base built once, K-step offsets added to the start-address
       // field (addr >> 4; smem addresses < 256 KB never carry out of 14 bits)
-      const uint64_t qdesc = sdesc_sw128(sq + t * C::kTileBytes, 16, 1024);
+      const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
       const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
       const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
-      const uint32_t tS = tmem + C::kTmemS + t * kBN;
-      const uint32_t tO = tmem + C::kTmemO + t * D;
-      auto issue_qk = [&](int r) {
-        uint64_t qd = qdesc;
+      auto issue_qk = [&](int t, int r) {
+        uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
         uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-        // opaque to the optimiser: stops the per-K-step descriptors being
+        // opaque to the optimiser: stops 2 x 8 per-K-step descriptors being
         // hoisted out of the K/V loop into (spilled) registers
         asm volatile("" : "+l"(qd), "+l"(kd));
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
-          umma_ss(tS, qd + off, kd + off, idesc_qk, ks > 0);
+          umma_ss(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
         }
         umma_commit(smem_u32(&bars->s_full[t]));
       };
       // PV in two halves of 64 keys, each issued as soon as the softmax
-      // warpgroup has written that half of P.
-      auto issue_pv = [&](int r, bool accumulate, int j) {
+      // warpgroup has written that half of P (P aliases S in TMEM).
+      auto issue_pv = [&](int t, int r, bool accumulate, int j) {
         uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
         asm volatile("" : "+l"(vd));
 #pragma unroll
@@ -221,7 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBN / 32; ++kk) {
             const int ks = h * (kBN / 32) + kk;
-            umma_ts(tO, tS + ks * 8, vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+            umma_ts(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
+                    vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
                     (accumulate || ks > 0) ? 1u : 0u);
           }
         }
@@ -231,22 +207,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(smem_u32(&bars->q_full), 0);
       tc_fence_after();
       wait_full(0);
-      issue_qk(0);
+      issue_qk(0, 0);
+      issue_qk(1, 0);
       release(0);
       for (int j = 1; j < n_kv; ++j) {
         const int rk = 2 * j, rv = 2 * j - 1;
         wait_full(rv);
-        if (t == 0) rec(kEvMmaWaitP0, j);
-        issue_pv(rv, j > 1, j - 1);
-        release(rv);
+        rec(kEvMmaWaitP0, j);
+        issue_pv(0, rv, j > 1, j - 1);
         wait_full(rk);
-        issue_qk(rk);
+        issue_qk(0, rk);
+        rec(kEvMmaIssuedPV0, j);
+        rec(kEvMmaWaitP1, j);
+        issue_pv(1, rv, j > 1, j - 1);
+        release(rv);
+        issue_qk(1, rk);
         release(rk);
-        if (t == 0) rec(kEvMmaIssuedPV0, j);
+        rec(kEvMmaIssuedPV1, j);
       }
       const int rv = 2 * n_kv - 1;
       wait_full(rv);
-      issue_pv(rv, n_kv > 1, n_kv - 1);
+      issue_pv(0, rv, n_kv > 1, n_kv - 1);
+      issue_pv(1, rv, n_kv > 1, n_kv - 1);
       release(rv);
     }
   }
@@ -347,11 +329,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           // emulated pairs are the last kEmuPer8/2 pairs of the group
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-#ifdef TA_DEBUG_NO_EXP  // timing ablation only: wrong results
-            if (true) {
-              f2_split(x[u], p[2 * u], p[2 * u + 1]);
-            } else
-#endif
             if (2 * u >= 8 - kEmuPer8) {
               ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
             } else {
