@@ -153,6 +153,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if (warp == kWarpMma - 1) {
+    // optional tracer: timestamps of tensor-core completions (diagnostics only)
+    if (lane == 0 && trace != nullptr) {
+      for (int j = 0; j < n_kv && j < kTraceIters; ++j) {
+        mbar_wait(smem_u32(&bars->o_full[0]), uint32_t(j & 1));
+        rec(kEvTcPV0Done, j);
+        if (j + 1 < n_kv) {
+          mbar_wait(smem_u32(&bars->s_full[0]), uint32_t((j + 1) & 1));
+          rec(kEvTcS0Done, j);
+        }
+        mbar_wait(smem_u32(&bars->o_full[1]), uint32_t(j & 1));
+        rec(kEvTcPV1Done, j);
+        if (j + 1 < n_kv) {
+          mbar_wait(smem_u32(&bars->s_full[1]), uint32_t((j + 1) & 1));
+          rec(kEvTcS1Done, j);
+        }
+      }
+    }
   } else if (warp == kWarpMma) {
     // ------------------------------------------------------------------ MMA
     if (lane == 0) {
