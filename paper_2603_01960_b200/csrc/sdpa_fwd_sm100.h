@@ -36,6 +36,10 @@ enum TraceEvent {
   kEvSm1Max,
   kEvSm1Exp,
   kEvSm1PArrive,
+  kEvTcPV0Done,  // tracer warp: o_full[0] phase j completed (PV0(j) done)
+  kEvTcS0Done,   // s_full[0] phase j+1 completed (S0(j+1) done)
+  kEvTcPV1Done,
+  kEvTcS1Done,
   kNumTraceEvents
 };
 
