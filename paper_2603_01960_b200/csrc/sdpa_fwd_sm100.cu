@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kWarpMma) {
     // ------------------------------------------------------------------ MMA
-    if (lane == 0) {
+    // The whole warp runs this loop (uniform control flow, descriptors in
+    // uniform registers); one elected lane issues each tcgen05 instruction.
+    {
       constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
       constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
       // ring position r (K_j at 2j, V_j at 2j+1) -> slot / phase
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
         tc_fence_after();
       };
-      auto release = [&](int r) { umma_commit(smem_u32(&bars->slot_empty[slot_of(r)])); };
+      auto release = [&](int r) { umma_commit_warp(smem_u32(&bars->slot_empty[slot_of(r)])); };
       // descriptors: base built once, K-step offsets added to the start-address
       // field (addr >> 4; smem addresses < 256 KB never carry out of 14 bits)
       const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
@@ -198,9 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
-          umma_ss(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
+          umma_ss_warp(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
         }
-        umma_commit(smem_u32(&bars->s_full[t]));
+        umma_commit_warp(smem_u32(&bars->s_full[t]));
       };
       // PV in two halves of 64 keys, each issued as soon as the softmax
       // warpgroup has written that half of P (P aliases S in TMEM).
@@ -214,12 +216,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBN / 32; ++kk) {
             const int ks = h * (kBN / 32) + kk;
-            umma_ts(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
+            umma_ts_warp(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
                     vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
                     (accumulate || ks > 0) ? 1u : 0u);
           }
         }
-        umma_commit(smem_u32(&bars->o_full[t]));
+        umma_commit_warp(smem_u32(&bars->o_full[t]));
       };
 
       mbar_wait(smem_u32(&bars->q_full), 0);
@@ -231,17 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 1; j < n_kv; ++j) {
         const int rk = 2 * j, rv = 2 * j - 1;
         wait_full(rv);
-        rec(kEvMmaWaitP0, j);
+        if (lane == 0) rec(kEvMmaWaitP0, j);
         issue_pv(0, rv, j > 1, j - 1);
         wait_full(rk);
         issue_qk(0, rk);
-        rec(kEvMmaIssuedPV0, j);
-        rec(kEvMmaWaitP1, j);
+        if (lane == 0) rec(kEvMmaIssuedPV0, j);
+        if (lane == 0) rec(kEvMmaWaitP1, j);
         issue_pv(1, rv, j > 1, j - 1);
         release(rv);
         issue_qk(1, rk);
         release(rk);
-        rec(kEvMmaIssuedPV1, j);
+        if (lane == 0) rec(kEvMmaIssuedPV1, j);
       }
       const int rv = 2 * n_kv - 1;
       wait_full(rv);
@@ -347,6 +349,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           // emulated pairs are the last kEmuPer8/2 pairs of the group
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
+#ifdef TA_DEBUG_NO_EXP  // timing ablation only: wrong results
+            if (true) {
+              f2_split(x[u], p[2 * u], p[2 * u + 1]);
+            } else
+#endif
             if (2 * u >= 8 - kEmuPer8) {
               ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
             } else {

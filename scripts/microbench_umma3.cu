@@ -8,7 +8,7 @@
 using namespace ta;
 constexpr int kGroups = 512;
 
-template <int G, int W, int C>
+template <int G, int W, int C, int KIND = 0>
 __global__ void __launch_bounds__(128, 1) bench(long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -29,7 +29,23 @@ __global__ void __launch_bounds__(128, 1) bench(long long* cycles) {
     const uint32_t idesc = make_idesc_f16(true, 128, 128, false, false);
     long long t0 = clock64();
     for (int g = 0; g < kGroups; ++g) {
-      for (int w = 0; w < W; ++w) { mbar_wait(smem_u32(&bar[1]), 0); tc_fence_after(); }
+      for (int w = 0; w < W; ++w) {
+        if (KIND == 0) { mbar_wait(smem_u32(&bar[1]), 0); tc_fence_after(); }
+        if (KIND == 1) { mbar_wait(smem_u32(&bar[1]), 0); }
+        if (KIND == 2) { tc_fence_after(); }
+        if (KIND == 3) {  // single try_wait probe, no loop
+          uint32_t ok;
+          asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+                       : "=r"(ok) : "r"(smem_u32(&bar[1])), "r"(0u) : "memory");
+          if (!ok) mbar_wait(smem_u32(&bar[1]), 0);
+        }
+        if (KIND == 4) {  // test_wait probe
+          uint32_t ok;
+          asm volatile("{\n\t.reg .pred P;\n\tmbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+                       : "=r"(ok) : "r"(smem_u32(&bar[1])), "r"(0u) : "memory");
+          if (!ok) mbar_wait(smem_u32(&bar[1]), 0);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < G; ++i) {
         const uint32_t ks = i & 7;
@@ -49,22 +65,22 @@ __global__ void __launch_bounds__(128, 1) bench(long long* cycles) {
   if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
-template <int G, int W, int C>
+template <int G, int W, int C, int KIND = 0>
 void run() {
   long long* cyc;
   cudaMalloc(&cyc, 148 * sizeof(long long));
   const int smem = 65536 + 2048;
-  cudaFuncSetAttribute(bench<G, W, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  bench<G, W, C><<<148, 128, smem>>>(cyc);
+  cudaFuncSetAttribute(bench<G, W, C, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench<G, W, C, KIND><<<148, 128, smem>>>(cyc);
   cudaDeviceSynchronize();
-  bench<G, W, C><<<148, 128, smem>>>(cyc);
+  bench<G, W, C, KIND><<<148, 128, smem>>>(cyc);
   cudaError_t e = cudaDeviceSynchronize();
   long long c[148];
   cudaMemcpy(c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += c[i];
   avg /= 148;
-  printf("group=%d waits/group=%d commits/group=%d : %7.2f cyc/MMA %s\n", G, W, C, avg / (kGroups * G),
+  printf("kind=%d group=%d waits/group=%d commits/group=%d : %7.2f cyc/MMA %s\n", KIND, G, W, C, avg / (kGroups * G),
          e == cudaSuccess ? "" : cudaGetErrorString(e));
   cudaFree(cyc);
 }
@@ -78,5 +94,11 @@ int main() {
   run<4, 1, 1>();
   run<4, 2, 1>();
   run<16, 2, 2>();
+  run<8, 2, 1, 1>();
+  run<8, 2, 1, 2>();
+  run<8, 2, 1, 3>();
+  run<8, 2, 1, 4>();
+  run<4, 2, 1, 1>();
+  run<4, 2, 1, 2>();
   return 0;
 }

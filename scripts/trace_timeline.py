@@ -11,18 +11,18 @@ q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=torch.bfloat16) for _ in
 o = torch.empty_like(q)
 for _ in range(3):
     ta.sdpa(q, k, v, out=o)
-tr = torch.zeros(14 * 64, dtype=torch.int64, device="cuda")
+tr = torch.zeros(18 * 64, dtype=torch.int64, device="cuda")
 L = ta.lib()
 L.ta_debug_sdpa_trace.restype = ctypes.c_int
 L.ta_debug_sdpa_trace.argtypes = [ctypes.c_void_p] * 4 + [ta._Shape, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
 ta._check(L.ta_debug_sdpa_trace(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), ta._Shape(B, H, S, D), ta.BF16, tr.data_ptr(), None))
-t = tr.view(14, 64).cpu().numpy()
-names = ["mmaWaitP0", "mmaIssPV0", "mmaWaitP1", "mmaIssPV1", "s0Ready", "s0Load", "s0Max", "s0Exp", "s0Arrive", "s1Ready", "s1Load", "s1Max", "s1Exp", "s1Arrive"]
+t = tr.view(18, 64).cpu().numpy()
+names = ["mmaWaitP0", "mmaIssPV0", "mmaWaitP1", "mmaIssPV1", "s0Ready", "s0Load", "s0Max", "s0Exp", "s0Arrive", "s1Ready", "s1Load", "s1Max", "s1Exp", "s1Arrive", "tcPV0", "tcS0", "tcPV1", "tcS1"]
 base = t[4, 0]
 n = min(64, (S + 127) // 128)
 print("iter " + " ".join(f"{x:>9s}" for x in names))
 for j in range(n):
-    print(f"{j:4d} " + " ".join(f"{(t[e, j] - base) if t[e, j] else 0:9d}" for e in range(14)))
+    print(f"{j:4d} " + " ".join(f"{(t[e, j] - base) if t[e, j] else 0:9d}" for e in range(18)))
 import numpy as np
 js = range(8, n - 1)
 def d(a, b): return np.mean([t[b, j] - t[a, j] for j in js])
@@ -33,3 +33,9 @@ print(" s1: ready->load %.0f load->max %.0f max->exp %.0f exp->arrive %.0f" % (d
 print(" s0 arrive(j) -> mma sees P0(j) [next iter]:", np.mean([t[0, j + 1] - t[8, j] for j in js]))
 print(" mma issued PV0,S0(j+1) -> s0 ready(j+1):", np.mean([t[4, j + 1] - t[1, j + 1] for j in js]))
 print(" s1 arrive(j) -> mma sees P1(j):", np.mean([t[2, j + 1] - t[13, j] for j in js]))
+print(" TC: PV0(j) done -> S0(j+1) done %.0f" % d(14, 15))
+print(" TC: S0(j+1) done -> PV1(j) done %.0f" % d(15, 16))
+print(" TC: PV1(j) done -> S1(j+1) done %.0f" % d(16, 17))
+print(" TC: S1(j+1) done -> PV0(j+1) done %.0f" % np.mean([t[14, j + 1] - t[17, j] for j in js]))
+print(" s0 P-half1 arrive(j) -> PV0(j) done %.0f" % np.mean([t[14, j] - t[8, j] for j in js]))
+print(" s1 P-half1 arrive(j) -> PV1(j) done %.0f" % np.mean([t[16, j] - t[13, j] for j in js]))
