@@ -31,18 +31,18 @@ namespace {
 constexpr int kBM = 128;        // rows per Q tile (UMMA M)
 constexpr int kBN = 128;        // keys per K/V tile (UMMA N of QK^T, K of PV)
 constexpr int kQTiles = 2;      // Q tiles per CTA (ping-pong)
-constexpr int kThreads = 640;   // 20 warps: 16 softmax + 4 control
+constexpr int kThreads = 384;   // 12 warps
 // Warp roles.  The SM's warp arbiter favours the highest warp id among
 // eligible warps, so the latency-critical single-thread roles (MMA issue, TMA)
 // take the top ids and are never starved by the softmax warps' issue stream.
-constexpr int kNumSoftmaxWarps = 16;  // warps 0..7 -> Q tile 0, 8..15 -> Q tile 1
-constexpr int kWarpAlloc = 16;        // TMEM allocator (otherwise idle)
-constexpr int kWarpTma = 17;
-constexpr int kWarpMma = 19;          // warp 18: optional tracer
+constexpr int kNumSoftmaxWarps = 8;  // warps 0..3 -> Q tile 0, 4..7 -> Q tile 1
+constexpr int kWarpAlloc = 8;        // TMEM allocator (otherwise idle)
+constexpr int kWarpTma = 9;
+constexpr int kWarpMma = 11;
 constexpr uint32_t kTmemCols = 512;
-// register split: 4 control warps (TMA, MMA, TMEM alloc, tracer) + 16 softmax warps
-constexpr int kRegsControl = 64;
-constexpr int kRegsSoftmax = 112;  // 128*64 + 512*112 <= 64K
+// register split: 4 control warps (TMA, MMA, TMEM alloc, spare) + 8 softmax warps
+constexpr int kRegsControl = 88;
+constexpr int kRegsSoftmax = 208;  // 128*88 + 256*208 <= 64K
 constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
@@ -61,12 +61,11 @@ struct Cfg {
   static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
   static constexpr int kSlots = D == 128 ? 4 : 8;           // K/V ring depth
   static constexpr int kSmemData = kQTiles * kTileBytes + kSlots * kTileBytes;
-  static constexpr int kSmemBytes = kSmemData + 9216 /*barriers + reductions*/ + 1024 /*align pad*/;
+  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/;
   static constexpr uint32_t kTmemS = 0;      // S0 at col 0, S1 at col 128 (fp32)
   static constexpr uint32_t kTmemO = 256;    // O0 at 256, O1 at 256 + D (fp32)
 };
 
-struct Barriers;
 struct Barriers {
   uint64_t q_full;
   uint64_t s_full[kQTiles];
@@ -75,10 +74,7 @@ struct Barriers {
   uint64_t slot_full[8];
   uint64_t slot_empty[8];
   uint32_t tmem_base;
-  alignas(16) float red[2048];  // softmax row-max exchange [2][2][2][128] + row sums [2][2][128]
 };
-
-static_assert(sizeof(Barriers) <= 9216, "barrier/reduction area overflows its smem budget");
 
 template <int D, bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -109,8 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&bars->q_full), 1);
     for (int t = 0; t < kQTiles; ++t) {
       mbar_init(smem_u32(&bars->s_full[t]), 1);
-      mbar_init(smem_u32(&bars->p_full[t][0]), 4);  // one arrive per lane-quadrant warp
-      mbar_init(smem_u32(&bars->p_full[t][1]), 4);
+      mbar_init(smem_u32(&bars->p_full[t][0]), kBM / 32);  // one arrive per warp
+      mbar_init(smem_u32(&bars->p_full[t][1]), kBM / 32);
       mbar_init(smem_u32(&bars->o_full[t]), 1);
     }
     for (int s = 0; s < C::kSlots; ++s) {
@@ -258,69 +254,54 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   } else {
     // -------------------------------------------------------------- softmax
-    // 8 warps per Q tile: warp w handles TMEM lane quadrant q = w % 4 (rows
-    // 32q..32q+31, one row per thread) and column half ch = (w / 4) % 2 of
-    // each 128-key S tile, i.e. two warps per SMSP per tile for latency
-    // hiding.  Row maxima are exchanged between the two column halves
-    // through shared memory; row sums are kept per half and combined at the
-    // end (both halves apply identical rescale factors).
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-    const int t = int(warp) / 8;
-    const int ch = (int(warp) / 4) & 1;
+    const int t = warp / 4;
     const uint32_t wq = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = int(wq * 32 + lane);
     const uint32_t lane_off = (wq * 32u) << 16;
-    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN + ch * 64;  // my 64 S columns
-    const uint32_t tP = tmem + lane_off + C::kTmemS + t * kBN + ch * 32;  // my 32 P columns
-    constexpr int kDh = D / 2;                                            // my O columns
-    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D + ch * kDh;
+    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN;
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
     const float sl2 = args.scale_log2;
     const uint32_t sbar = smem_u32(&bars->s_full[t]);
     const uint32_t obar = smem_u32(&bars->o_full[t]);
-    const uint32_t pbar = smem_u32(&bars->p_full[t][ch]);
-    const uint32_t pair_bar = 1 + t * 4 + wq;  // named barrier of the two column-half warps
-    float* red = reinterpret_cast<float*>(bars->red);  // [2 parity][2 t][2 ch][128 rows]
-    const bool tr = (row == 0) && ch == 0;
 
     float m_run = -INFINITY;  // running max used for the exponent (scaled, log2 units)
-    float l_run = 0.f;        // running normaliser of my column half, relative to m_run
+    float l_run = 0.f;        // running normaliser relative to m_run
 
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(sbar, uint32_t(j & 1));
       tc_fence_after();
+      const bool tr = (row == 0);
       if (tr) rec(kEvSm0SReady + 5 * t, j);
-      uint32_t sr[2][32];
-      tmem_ld32(tS, sr[0]);
-      tmem_ld32(tS + 32, sr[1]);
-      tmem_wait_ld();
-      reg_fence(sr[0]);
-      reg_fence(sr[1]);
-      if (tr) rec(kEvSm0Loaded + 5 * t, j);
-      float s[64];
+      uint32_t sr[4][32];
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
+      if (tr) rec(kEvSm0Loaded + 5 * t, j);
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
 
       if (j == n_kv - 1) {
-        const int valid = S - j * kBN - ch * 64;  // keys past S were zero-filled by TMA
-        if (valid < 64) {
+        const int valid = S - j * kBN;  // keys past S were zero-filled by TMA
+        if (valid < kBN) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
+          for (int i = 0; i < 128; ++i)
             if (i >= valid) s[i] = -INFINITY;
         }
       }
-      // partial row max over my 64 columns, then exchange with the partner warp
-      float mx4[4];
+      // row max (8 independent chains)
+      float mx8[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) mx4[i] = s[i];
+      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
 #pragma unroll
-      for (int i = 4; i < 64; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
-      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      float* redj = red + (j & 1) * 512 + t * 256;
-      redj[ch * 128 + row] = mx;
-      named_bar_sync(pair_bar, 64);
-      mx = fmaxf(mx, redj[(ch ^ 1) * 128 + row]);
+      for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float m_new = mx * sl2;
       if (tr) rec(kEvSm0Max + 5 * t, j);
       const bool need = m_new > m_run + kRescaleThreshold;
@@ -328,6 +309,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (need) {
         l_run *= alpha;
         m_run = m_new;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // O correction (rare with the lazy threshold): wait until PV(j-1) has
+        // landed in TMEM and rescale in place; PV(j) is not issued before this
+        // warpgroup signals the first half of P(j).
+        mbar_wait(obar, uint32_t((j - 1) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orow[32];
+          tmem_ld32(tO + c * 32, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+          tmem_st32(tO + c * 32, orow);
+        }
       }
       const float m_use = m_run == -INFINITY ? 0.f : m_run;
       // x = s * scale*log2e - m as packed FFMA2; exp2 split between the MUFU
@@ -337,17 +336,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t negm2 = f2(-m_use, -m_use);
       uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-      uint32_t pk[32];
-#pragma unroll
       for (int h = 0; h < 2; ++h) {
+        uint32_t pk[32];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {  // groups of 8 columns
-          const int c0 = h * 32 + g * 8;
+        for (int g = 0; g < 8; ++g) {  // groups of 8 columns
+          const int c0 = h * 64 + g * 8;
           uint64_t x[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
           float p[8];
+          // emulated pairs are the last kEmuPer8/2 pairs of the group
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
 #ifdef TA_DEBUG_NO_EXP  // timing ablation only: wrong results
@@ -367,34 +366,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
-            pk[h * 16 + g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+            pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
           }
         }
+        tmem_st32(tS + h * 32, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
+        if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
       }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // O correction (rare with the lazy threshold) on my O columns: wait
-        // until PV(j-1) has landed in TMEM, rescale in place; PV(j) is not
-        // issued before both halves of P(j) are signalled below.
-        mbar_wait(obar, uint32_t((j - 1) & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < kDh / 16; ++c) {
-          uint32_t orow[16];
-          tmem_ld16(tO + c * 16, orow);
-          tmem_wait_ld();
-          reg_fence(orow);
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
-          tmem_st16(tO + c * 16, orow);
-        }
-      }
-      tmem_st32(tP, pk);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(pbar);
-      if (tr) rec(kEvSm0Exp + 5 * t, j);
       {
         const uint64_t a01 = fadd2(acc[0], acc[1]);
         const uint64_t a23 = fadd2(acc[2], acc[3]);
@@ -406,21 +387,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ------------------------------------------------------------- epilogue
-    // combine the two column halves' normalisers
-    {
-      float* redl = red + 1024 + t * 256;
-      redl[ch * 128 + row] = l_run;
-      named_bar_sync(pair_bar, 64);
-      l_run += redl[(ch ^ 1) * 128 + row];
-    }
     mbar_wait(obar, uint32_t((n_kv - 1) & 1));
     tc_fence_after();
     const int grow = q0 + t * kBM + row;
     const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-    uint16_t* orow_g =
-        reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D + ch * kDh;
+    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
 #pragma unroll
-    for (int c = 0; c < kDh / 32; ++c) {
+    for (int c = 0; c < D / 32; ++c) {
       uint32_t orow[32];
       tmem_ld32(tO + c * 32, orow);
       tmem_wait_ld();
@@ -438,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               packed[4 * i + 3]);
       }
     }
-    if (ch == 0 && args.lse != nullptr && grow < S)
+    if (args.lse != nullptr && grow < S)
       args.lse[size_t(bh) * S + grow] =
           l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
   }
