@@ -41,8 +41,15 @@ constexpr int kWarpTma = 9;
 constexpr int kWarpMma = 11;
 constexpr uint32_t kTmemCols = 512;
 // register split: 4 control warps (TMA, MMA, TMEM alloc, spare) + 8 softmax warps
+// setmaxnreg.inc only draws on registers released by setmaxnreg.dec in the
+// same CTA, so the split must balance around the launch allocation
+// (65536 / 384 threads -> 168 per thread): 256*(208-168) == 128*(168-88).
+constexpr int kLaunchRegs = (65536 / kThreads) & ~7;
 constexpr int kRegsControl = 88;
-constexpr int kRegsSoftmax = 208;  // 128*88 + 256*208 <= 64K
+constexpr int kRegsSoftmax = 208;
+static_assert(kNumSoftmaxWarps * 32 * (kRegsSoftmax - kLaunchRegs) <=
+                  (kThreads - kNumSoftmaxWarps * 32) * (kLaunchRegs - kRegsControl),
+              "setmaxnreg.inc would wait forever: register pool does not balance");
 constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
@@ -50,7 +57,7 @@ constexpr float kRescaleThreshold = 8.0f;
 // exp2 work split: of every 8 score columns, kEmuPer8 use the FMA-pipe
 // polynomial (ex2_poly) and the rest the MUFU (measured 16 exp2/clk/SM).
 #ifndef TA_EMU_PER8
-#define TA_EMU_PER8 0
+#define TA_EMU_PER8 2
 #endif
 constexpr int kEmuPer8 = TA_EMU_PER8;
 
