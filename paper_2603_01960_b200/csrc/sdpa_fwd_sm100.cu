@@ -60,6 +60,11 @@ constexpr float kRescaleThreshold = 8.0f;
 #define TA_EMU_PER8 2
 #endif
 constexpr int kEmuPer8 = TA_EMU_PER8;
+// P hand-off granularity to the PV MMAs (2 = halves, 4 = quarters of 32 keys)
+#ifndef TA_P_PARTS
+#define TA_P_PARTS 4
+#endif
+constexpr int kPParts = TA_P_PARTS;
 
 template <int D>
 struct Cfg {
@@ -76,7 +81,7 @@ struct Cfg {
 struct Barriers {
   uint64_t q_full;
   uint64_t s_full[kQTiles];
-  uint64_t p_full[kQTiles][2];  // P columns [0,64) / [64,128) written
+  uint64_t p_full[kQTiles][4];  // P key columns [32q, 32q+32) written (q < kPParts)
   uint64_t o_full[kQTiles];
   uint64_t slot_full[8];
   uint64_t slot_empty[8];
@@ -112,8 +117,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&bars->q_full), 1);
     for (int t = 0; t < kQTiles; ++t) {
       mbar_init(smem_u32(&bars->s_full[t]), 1);
-      mbar_init(smem_u32(&bars->p_full[t][0]), kBM / 32);  // one arrive per warp
-      mbar_init(smem_u32(&bars->p_full[t][1]), kBM / 32);
+      for (int q = 0; q < kPParts; ++q)
+        mbar_init(smem_u32(&bars->p_full[t][q]), kBM / 32);  // one arrive per warp
       mbar_init(smem_u32(&bars->o_full[t]), 1);
     }
     for (int s = 0; s < C::kSlots; ++s) {
@@ -217,12 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
         asm volatile("" : "+l"(vd));
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kPParts; ++h) {
           mbar_wait(smem_u32(&bars->p_full[t][h]), uint32_t(j & 1));
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < kBN / 32; ++kk) {
-            const int ks = h * (kBN / 32) + kk;
+          for (int kk = 0; kk < kBN / 16 / kPParts; ++kk) {
+            const int ks = h * (kBN / 16 / kPParts) + kk;
             umma_ts_warp(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
                     vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
                     (accumulate || ks > 0) ? 1u : 0u);
@@ -343,11 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t negm2 = f2(-m_use, -m_use);
       uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t pk[32];
+      for (int h = 0; h < kPParts; ++h) {
+        constexpr int kCols = kBN / kPParts;  // key columns per P part
+        uint32_t pk[kCols / 32][16];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {  // groups of 8 columns
-          const int c0 = h * 64 + g * 8;
+        for (int g = 0; g < kCols / 8; ++g) {  // groups of 8 columns
+          const int c0 = h * kCols + g * 8;
           uint64_t x[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -373,10 +379,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
-            pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+            pk[(g * 4 + u) / 16][(g * 4 + u) % 16] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
           }
         }
-        tmem_st32(tS + h * 32, pk);
+#pragma unroll
+        for (int i = 0; i < kCols / 32; ++i) tmem_st16(tS + h * (kCols / 2) + i * 16, pk[i]);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
