@@ -61,10 +61,10 @@ constexpr float kRescaleThreshold = 8.0f;
 #endif
 constexpr int kEmuPer8 = TA_EMU_PER8;
 // P hand-off granularity to the PV MMAs (2 = halves, 4 = quarters of 32 keys)
-#ifndef TA_P_PARTS
-#define TA_P_PARTS 4
-#endif
-constexpr int kPParts = TA_P_PARTS;
+// (halves: the rescale slow path relies on the o_half barrier)
+constexpr int kPParts = 2;
+// lazy-rescale guard on the per-half row sum (see the softmax loop)
+constexpr float kSumGuard = 256.0f;
 
 template <int D>
 struct Cfg {
@@ -83,6 +83,7 @@ struct Barriers {
   uint64_t s_full[kQTiles];
   uint64_t p_full[kQTiles][4];  // P key columns [32q, 32q+32) written (q < kPParts)
   uint64_t o_full[kQTiles];
+  uint64_t o_half[kQTiles];  // PV(j) over P columns [0,64) complete
   uint64_t slot_full[8];
   uint64_t slot_empty[8];
   uint32_t tmem_base;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int q = 0; q < kPParts; ++q)
         mbar_init(smem_u32(&bars->p_full[t][q]), kBM / 32);  // one arrive per warp
       mbar_init(smem_u32(&bars->o_full[t]), 1);
+      mbar_init(smem_u32(&bars->o_half[t]), 1);
     }
     for (int s = 0; s < C::kSlots; ++s) {
       mbar_init(smem_u32(&bars->slot_full[s]), 1);
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
                     (accumulate || ks > 0) ? 1u : 0u);
           }
+          if (h == 0) umma_commit_warp(smem_u32(&bars->o_half[t]));
         }
         umma_commit_warp(smem_u32(&bars->o_full[t]));
       };
@@ -280,6 +283,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_run = -INFINITY;  // running max used for the exponent (scaled, log2 units)
     float l_run = 0.f;        // running normaliser relative to m_run
 
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    const uint32_t ohbar = smem_u32(&bars->o_half[t]);
+    // exp2 of one 64-key half against m_use: packed FFMA2 for
+    // x = s*scale*log2e - m, exp2 split between the MUFU and the FMA pipe
+    // (kEmuPer8 of every 8 columns, emulated in pairs), row sum as packed
+    // FADD2, P packed to 16-bit for the TS-MMA.
+    auto exp_part = [&](const float (&s)[128], int h, float m_use, uint32_t (&pk)[2][16],
+                        float& sum) {
+      const uint64_t negm2 = f2(-m_use, -m_use);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {  // groups of 8 columns
+        const int c0 = h * 64 + g * 8;
+        uint64_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
+        float p[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#ifdef TA_DEBUG_NO_EXP  // timing ablation only: wrong results
+          if (true) {
+            f2_split(x[u], p[2 * u], p[2 * u + 1]);
+          } else
+#endif
+          if (2 * u >= 8 - kEmuPer8) {
+            ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
+          } else {
+            float a, b;
+            f2_split(x[u], a, b);
+            p[2 * u] = ex2(a);
+            p[2 * u + 1] = ex2(b);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
+          pk[g / 4][(g % 4) * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+        }
+      }
+      const uint64_t a01 = fadd2(acc[0], acc[1]);
+      const uint64_t a23 = fadd2(acc[2], acc[3]);
+      float lo, hi;
+      f2_split(fadd2(a01, a23), lo, hi);
+      sum = lo + hi;
+    };
+
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(sbar, uint32_t(j & 1));
       tc_fence_after();
@@ -306,96 +356,71 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (i >= valid) s[i] = -INFINITY;
         }
       }
-      // row max (8 independent chains)
-      float mx8[8];
+      if (j == 0) {
+        // first tile: the running max starts from the tile's row max
+        float mx4[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+        for (int i = 0; i < 4; ++i) mx4[i] = s[i];
 #pragma unroll
-      for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float m_new = mx * sl2;
+        for (int i = 4; i < 128; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+        m_run = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+      }
       if (tr) rec(kEvSm0Max + 5 * t, j);
-      const bool need = m_new > m_run + kRescaleThreshold;
-      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
-      if (need) {
-        l_run *= alpha;
-        m_run = m_new;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // O correction (rare with the lazy threshold): wait until PV(j-1) has
-        // landed in TMEM and rescale in place; PV(j) is not issued before this
-        // warpgroup signals the first half of P(j).
-        mbar_wait(obar, uint32_t((j - 1) & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t orow[32];
-          tmem_ld32(tO + c * 32, orow);
-          tmem_wait_ld();
-          reg_fence(orow);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
-          tmem_st32(tO + c * 32, orow);
-        }
-      }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      // x = s * scale*log2e - m as packed FFMA2; exp2 split between the MUFU
-      // and the FMA pipe (kEmuPer8 of every 8 columns, emulated in pairs);
-      // row sum as packed FADD2 into 4 pair accumulators.
-      const uint64_t sl2x2 = f2(sl2, sl2);
-      const uint64_t negm2 = f2(-m_use, -m_use);
-      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+      // Later tiles exponentiate against the running max directly (no
+      // per-tile max reduction on the critical path).  The lazy-rescale
+      // invariant p <= 2^kRescaleThreshold is guarded by the row sum (any
+      // p > 2^8 implies sum > 2^8); only then (rare) is the half's true max
+      // taken and O / l rescaled.
 #pragma unroll
       for (int h = 0; h < kPParts; ++h) {
-        constexpr int kCols = kBN / kPParts;  // key columns per P part
-        uint32_t pk[kCols / 32][16];
+        uint32_t pk[2][16];
+        float sum;
+        exp_part(s, h, m_run == -INFINITY ? 0.f : m_run, pk, sum);
+        if (__any_sync(0xffffffffu, sum > kSumGuard)) {
+          float hm4[4];
 #pragma unroll
-        for (int g = 0; g < kCols / 8; ++g) {  // groups of 8 columns
-          const int c0 = h * kCols + g * 8;
-          uint64_t x[4];
+          for (int i = 0; i < 4; ++i) hm4[i] = s[h * 64 + i];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
-          float p[8];
-          // emulated pairs are the last kEmuPer8/2 pairs of the group
+          for (int i = 4; i < 64; ++i) hm4[i & 3] = fmaxf(hm4[i & 3], s[h * 64 + i]);
+          const float m_half = fmaxf(fmaxf(hm4[0], hm4[1]), fmaxf(hm4[2], hm4[3])) * sl2;
+          const bool need = sum > kSumGuard && m_half > m_run;
+          const float alpha = need ? ex2(m_run - m_half) : 1.f;
+          if (need) {
+            l_run *= alpha;
+            m_run = m_half;
+          }
+          // O must be stable before rescaling: PV(j-1) for the first half,
+          // PV(j) over the first half of P for the second (neither part of
+          // P(j) at or after this one has been signalled yet).
+          if (h == 0) {
+            if (j > 0) mbar_wait(obar, uint32_t((j - 1) & 1));
+          } else {
+            mbar_wait(ohbar, uint32_t(j & 1));
+          }
+          tc_fence_after();
+          if (h == 1 || j > 0) {
+#pragma unroll 1
+            for (int c = 0; c < D / 16; ++c) {
+              uint32_t orow[16];
+              tmem_ld16(tO + c * 16, orow);
+              tmem_wait_ld();
+              reg_fence(orow);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-#ifdef TA_DEBUG_NO_EXP  // timing ablation only: wrong results
-            if (true) {
-              f2_split(x[u], p[2 * u], p[2 * u + 1]);
-            } else
-#endif
-            if (2 * u >= 8 - kEmuPer8) {
-              ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
-            } else {
-              float a, b;
-              f2_split(x[u], a, b);
-              p[2 * u] = ex2(a);
-              p[2 * u + 1] = ex2(b);
+              for (int i = 0; i < 16; ++i)
+                orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+              tmem_st16(tO + c * 16, orow);
             }
           }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
-            pk[(g * 4 + u) / 16][(g * 4 + u) % 16] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
-          }
+          exp_part(s, h, m_run == -INFINITY ? 0.f : m_run, pk, sum);
         }
-#pragma unroll
-        for (int i = 0; i < kCols / 32; ++i) tmem_st16(tS + h * (kCols / 2) + i * 16, pk[i]);
+        l_run += sum;
+        tmem_st16(tS + h * 32, pk[0]);
+        tmem_st16(tS + h * 32 + 16, pk[1]);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
         if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
-      }
-      {
-        const uint64_t a01 = fadd2(acc[0], acc[1]);
-        const uint64_t a23 = fadd2(acc[2], acc[3]);
-        float lo, hi;
-        f2_split(fadd2(a01, a23), lo, hi);
-        l_run += lo + hi;
       }
       if (tr) rec(kEvSm0PArrive + 5 * t, j);
     }
