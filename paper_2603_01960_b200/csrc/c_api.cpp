@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -247,11 +248,30 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   return TA_OK;
 }
 
-// per-device workspace for the host-buffer entry
+// per-device workspace for the host-buffer entry: device buffers plus the
+// copy streams / events of the chunked H2D -> compute -> D2H pipeline
 struct Workspace {
+  static constexpr int kMaxChunks = 16;
   std::mutex mu;
   void* ptr = nullptr;
   size_t bytes = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
+  cudaEvent_t ev_compute_done = nullptr;
+
+  ta_status ensure_streams() {
+    if (h2d) return TA_OK;
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ev_compute_done, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "workspace streams");
+    for (int i = 0; i < kMaxChunks; ++i)
+      if ((e = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "workspace events");
+    return TA_OK;
+  }
 };
 
 Workspace& workspace(int dev) {
@@ -350,26 +370,59 @@ ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o,
     ws.bytes = need;
   }
   char* base = static_cast<char*>(ws.ptr);
-  void* dq = base;
-  void* dk = base + tbytes;
-  void* dv = base + 2 * tbytes;
-  void* dout = base + 3 * tbytes;
+  char* dq = base;
+  char* dk = base + tbytes;
+  char* dv = base + 2 * tbytes;
+  char* dout = base + 3 * tbytes;
   float* dl = lse ? reinterpret_cast<float*>(base + 4 * tbytes) : nullptr;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
-  if ((e = cudaMemcpyAsync(dq, q, n * 2, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(dk, k, n * 2, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(dv, v, n * 2, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-    return cuda_fail(e, "H2D copy");
   auto plan = get_plan(sched, shape.d, dtype, mask == TA_MASK_CAUSAL);
-  if ((st = run_device(dq, dk, dv, dout, dl, shape, dtype, eff, *plan, stream)) != TA_OK)
-    return st;
-  if ((e = cudaMemcpyAsync(o, dout, n * 2, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return cuda_fail(e, "D2H copy");
-  if (lse &&
-      (e = cudaMemcpyAsync(lse, dl, size_t(shape.b * shape.h * shape.s) * 4,
-                           cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return cuda_fail(e, "D2H copy");
+  // Pipeline over head chunks: H2D of chunk c+1 and D2H of chunk c-1 run on
+  // the workspace's copy streams while chunk c computes on the caller's
+  // stream (heads are independent and contiguous in [B*H, S, D]).
+  const int64_t bh = shape.b * shape.h;
+  const size_t head_elems = size_t(shape.s * shape.d);
+  const int n_chunks = int(n * 2 >= (size_t(64) << 20) ? std::min<int64_t>(bh, 16) : 1);
+  if ((st = ws.ensure_streams()) != TA_OK) return st;
+  int64_t h0 = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int64_t h1 = bh * (c + 1) / n_chunks;
+    const int64_t hc = h1 - h0;
+    if (hc == 0) continue;
+    const size_t off = size_t(h0) * head_elems * 2, bytes = size_t(hc) * head_elems * 2;
+    // inputs of this chunk, ordered after the previous call's use of the
+    // workspace (the compute stream's last event)
+    if ((e = cudaStreamWaitEvent(ws.h2d, ws.ev_compute_done, 0)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dq + off, static_cast<const char*>(q) + off, bytes,
+                             cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dk + off, static_cast<const char*>(k) + off, bytes,
+                             cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dv + off, static_cast<const char*>(v) + off, bytes,
+                             cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
+        (e = cudaEventRecord(ws.ev_in[c], ws.h2d)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, ws.ev_in[c], 0)) != cudaSuccess)
+      return cuda_fail(e, "H2D copy");
+    const ta_shape cs{1, hc, shape.s, shape.d};
+    if ((st = run_device(dq + off, dk + off, dv + off, dout + off,
+                         dl ? dl + size_t(h0) * size_t(shape.s) : nullptr, cs, dtype, eff, *plan,
+                         stream)) != TA_OK)
+      return st;
+    if ((e = cudaEventRecord(ws.ev_out[c], s)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(ws.d2h, ws.ev_out[c], 0)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(static_cast<char*>(o) + off, dout + off, bytes,
+                             cudaMemcpyDeviceToHost, ws.d2h)) != cudaSuccess)
+      return cuda_fail(e, "D2H copy");
+    if (lse &&
+        (e = cudaMemcpyAsync(lse + size_t(h0) * size_t(shape.s), dl + size_t(h0) * size_t(shape.s),
+                             size_t(hc) * size_t(shape.s) * 4, cudaMemcpyDeviceToHost,
+                             ws.d2h)) != cudaSuccess)
+      return cuda_fail(e, "D2H copy");
+    h0 = h1;
+  }
+  if ((e = cudaEventRecord(ws.ev_compute_done, s)) != cudaSuccess)
+    return cuda_fail(e, "event record");
+  if ((e = cudaStreamSynchronize(ws.d2h)) != cudaSuccess) return cuda_fail(e, "D2H sync");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
   fill_stats(stats, *plan, shape);
   return TA_OK;
