@@ -236,8 +236,10 @@ def sdpa_numpy(q, k, v, scale=None, causal=False, valid_len=None):
         idx = np.arange(S)
         s = np.where(idx[None, :] <= idx[:, None], s, -np.inf)
     if valid_len is not None:
-        B = q.shape[0]
-        vl = np.asarray(valid_len).reshape(B, *([1] * (q.ndim - 1)))
+        if q.ndim == 2:  # one head: a single key-side length
+            vl = int(np.asarray(valid_len).ravel()[0])
+        else:            # [B, H, S, D]: one length per batch
+            vl = np.asarray(valid_len).reshape(q.shape[0], *([1] * (q.ndim - 1)))
         s = np.where(np.arange(S) < vl, s, -np.inf)
     m = s.max(axis=-1, keepdims=True)
     finite = np.isfinite(m)

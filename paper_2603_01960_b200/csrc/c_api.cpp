@@ -87,8 +87,9 @@ ta_status validate_device_support(ta_shape sh, ta_dtype dt, ta_mask_kind mask) {
   if (sh.d != 64 && sh.d != 128)
     return fail(TA_ERR_UNSUPPORTED, "head dim " + std::to_string(sh.d) +
                                         " not supported (D in {64,128})");
-  if (mask != TA_MASK_NONE)
-    return fail(TA_ERR_UNSUPPORTED, "mask kind not yet supported on the sm_100a path");
+  if (mask == TA_MASK_PADDING && sh.b > ta::kMaxPaddingBatch)
+    return fail(TA_ERR_UNSUPPORTED, "padding masks support B <= " +
+                                        std::to_string(ta::kMaxPaddingBatch));
   if (sh.s > (int64_t(1) << 30)) return fail(TA_ERR_UNSUPPORTED, "S too large");
   if (sh.b * sh.h > 65535) return fail(TA_ERR_UNSUPPORTED, "B*H > 65535");
   return TA_OK;
@@ -203,13 +204,30 @@ ta_status check_device() {
   return TA_OK;
 }
 
-void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh) {
+// KernelStats::kv_tiles_visited (tiled.hpp:246-257) for the executed 128-row
+// query tiles: causal visits kv_end = last_row / t_n + 1 tiles (tiled.cpp:159),
+// padding ceil(valid_len / t_n).
+void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh, ta_mask_kind mask,
+                const int64_t* valid_len) {
   if (!st) return;
   const int64_t bh = sh.b * sh.h;
   const int64_t q_tiles = (sh.s + p.block_m - 1) / p.block_m;
   const int64_t kv_tiles = (sh.s + p.block_n - 1) / p.block_n;
   const auto g = ta::fwd_geometry(sh.s, bh);
-  st->kv_tiles_visited = uint64_t(bh * q_tiles * kv_tiles);
+  uint64_t visited = 0;
+  if (mask == TA_MASK_CAUSAL) {
+    for (int64_t qt = 0; qt < q_tiles; ++qt) {
+      const int64_t last = std::min<int64_t>((qt + 1) * p.block_m, sh.s) - 1;
+      visited += uint64_t(last / p.block_n + 1);
+    }
+    visited *= uint64_t(bh);
+  } else if (mask == TA_MASK_PADDING) {
+    for (int64_t b = 0; b < sh.b; ++b)
+      visited += uint64_t(sh.h * q_tiles * ((valid_len[b] + p.block_n - 1) / p.block_n));
+  } else {
+    visited = uint64_t(bh * q_tiles * kv_tiles);
+  }
+  st->kv_tiles_visited = visited;
   st->block_m = p.block_m;
   st->block_n = p.block_n;
   st->stages = p.stages;
@@ -219,9 +237,17 @@ void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh) {
   st->reserved = 0;
 }
 
+struct MaskArgs {
+  ta_mask_kind kind = TA_MASK_NONE;
+  const int64_t* valid_len = nullptr;  // host, [B] (padding)
+  int64_t heads = 1;                   // H of the caller's [B,H,S,D] view
+  int64_t bh_offset = 0;               // first flattened head of this launch
+  int64_t batches = 1;
+};
+
 ta_status run_device(const void* q, const void* k, const void* v, void* o, float* lse,
                      ta_shape sh, ta_dtype dt, double scale, const Plan& plan, void* stream,
-                     long long* trace = nullptr) {
+                     const MaskArgs& mask_args, long long* trace = nullptr) {
   const bool bf16 = dt == TA_BF16;
   const int64_t bh = sh.b * sh.h;
   CUtensorMap mq, mk, mv;
@@ -238,6 +264,12 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.args.seq_len = int(sh.s);
   L.args.scale_log2 = float(scale * 1.4426950408889634074);
   L.args.trace = trace;
+  L.args.mask = int(mask_args.kind);
+  L.args.heads = int(mask_args.heads);
+  L.args.bh_offset = int(mask_args.bh_offset);
+  if (mask_args.kind == TA_MASK_PADDING)
+    for (int64_t b = 0; b < mask_args.batches; ++b)
+      L.args.valid_len[b] = int(mask_args.valid_len[b]);
   L.bh = bh;
   L.head_dim = int(sh.d);
   L.bf16 = bf16;
@@ -334,8 +366,10 @@ ta_status ta_sdpa_fwd(const void* q, const void* k, const void* v, void* o, floa
     return fail(TA_ERR_INVALID_ARGUMENT, "q/k/v/o must be 16-byte aligned");
   if ((st = check_device()) != TA_OK) return st;
   auto plan = get_plan(sched, shape.d, dtype, mask == TA_MASK_CAUSAL);
-  if ((st = run_device(q, k, v, o, lse, shape, dtype, eff, *plan, stream)) != TA_OK) return st;
-  fill_stats(stats, *plan, shape);
+  MaskArgs mk{mask, valid_len, shape.h, 0, shape.b};
+  if ((st = run_device(q, k, v, o, lse, shape, dtype, eff, *plan, stream, mk)) != TA_OK)
+    return st;
+  fill_stats(stats, *plan, shape, mask, valid_len);
   return TA_OK;
 }
 
@@ -404,9 +438,10 @@ ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o,
         (e = cudaStreamWaitEvent(s, ws.ev_in[c], 0)) != cudaSuccess)
       return cuda_fail(e, "H2D copy");
     const ta_shape cs{1, hc, shape.s, shape.d};
+    MaskArgs mk{mask, valid_len, shape.h, h0, shape.b};
     if ((st = run_device(dq + off, dk + off, dv + off, dout + off,
                          dl ? dl + size_t(h0) * size_t(shape.s) : nullptr, cs, dtype, eff, *plan,
-                         stream)) != TA_OK)
+                         stream, mk)) != TA_OK)
       return st;
     if ((e = cudaEventRecord(ws.ev_out[c], s)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(ws.d2h, ws.ev_out[c], 0)) != cudaSuccess ||
@@ -424,7 +459,7 @@ ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o,
     return cuda_fail(e, "event record");
   if ((e = cudaStreamSynchronize(ws.d2h)) != cudaSuccess) return cuda_fail(e, "D2H sync");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
-  fill_stats(stats, *plan, shape);
+  fill_stats(stats, *plan, shape, mask, valid_len);
   return TA_OK;
 }
 
@@ -437,7 +472,8 @@ ta_status ta_debug_sdpa_trace(const void* q, const void* k, const void* v, void*
   if ((st = validate_device_support(shape, dtype, TA_MASK_NONE)) != TA_OK) return st;
   if ((st = check_device()) != TA_OK) return st;
   auto plan = get_plan(sched, shape.d, dtype, false);
-  if ((st = run_device(q, k, v, o, nullptr, shape, dtype, eff, *plan, stream, trace)) != TA_OK)
+  if ((st = run_device(q, k, v, o, nullptr, shape, dtype, eff, *plan, stream, MaskArgs{},
+                       trace)) != TA_OK)
     return st;
   cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "trace sync");

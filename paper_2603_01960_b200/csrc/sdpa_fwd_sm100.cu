@@ -105,8 +105,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = lane_id();
   const int S = args.seq_len;
   const int bh = blockIdx.y;
-  const int q0 = blockIdx.x * (kBM * kQTiles);
-  const int n_kv = (S + kBN - 1) / kBN;
+  // causal: heaviest query blocks first (longest-processing-time order)
+  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
+  const int q0 = qblk * (kBM * kQTiles);
+  // keys admitted by the mask (reference MaskSpec::admits, types.hpp:48-67):
+  // None -> j < S; Padding -> j < valid_len[b]; Causal -> j <= i, which also
+  // bounds the K/V tiles a query tile visits (kv_end = last_row / t_n + 1,
+  // tiled.cpp:159).  n_kv_t[t] is the trip count of Q tile t.
+  const int kv_len =
+      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
+  const int n_kv_seq = (kv_len + kBN - 1) / kBN;
+  const int diag0 = q0 / kBN;  // K/V tile on Q tile 0's diagonal
+  int n_kv_t[kQTiles];
+#pragma unroll
+  for (int t = 0; t < kQTiles; ++t)
+    n_kv_t[t] = args.mask == kMaskCausal ? min(diag0 + t + 1, n_kv_seq) : n_kv_seq;
+  const int n_kv = n_kv_t[kQTiles - 1];  // K/V tiles streamed (max over the Q tiles)
   long long* const trace =
       (args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
   auto rec = [&](int ev, int j) {
@@ -142,8 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
       const uint32_t qbar = smem_u32(&bars->q_full);
-      mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
-      for (int t = 0; t < kQTiles; ++t)
+      if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
+      for (int t = 0; t < kQTiles && n_kv > 0; ++t)  // (no key admitted: Q unused)
         for (int r = 0; r < C::kRegions; ++r)
           tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
                       q0 + t * kBM, bh);
@@ -236,32 +250,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit_warp(smem_u32(&bars->o_full[t]));
       };
 
-      mbar_wait(smem_u32(&bars->q_full), 0);
-      tc_fence_after();
-      wait_full(0);
-      issue_qk(0, 0);
-      issue_qk(1, 0);
-      release(0);
-      for (int j = 1; j < n_kv; ++j) {
-        const int rk = 2 * j, rv = 2 * j - 1;
+      // Q tile 0 visits n0 <= n1 K/V tiles (fewer under the causal mask)
+      const int n0 = n_kv_t[0], n1 = n_kv_t[1];
+      if (n1 > 0) {
+        mbar_wait(smem_u32(&bars->q_full), 0);
+        tc_fence_after();
+        wait_full(0);
+        if (n0 > 0) issue_qk(0, 0);
+        issue_qk(1, 0);
+        release(0);
+        for (int j = 1; j < n1; ++j) {
+          const int rk = 2 * j, rv = 2 * j - 1;
+          wait_full(rv);
+          if (lane == 0) rec(kEvMmaWaitP0, j);
+          if (j - 1 < n0) issue_pv(0, rv, j > 1, j - 1);
+          wait_full(rk);
+          if (j < n0) issue_qk(0, rk);
+          if (lane == 0) rec(kEvMmaIssuedPV0, j);
+          if (lane == 0) rec(kEvMmaWaitP1, j);
+          issue_pv(1, rv, j > 1, j - 1);
+          release(rv);
+          issue_qk(1, rk);
+          release(rk);
+          if (lane == 0) rec(kEvMmaIssuedPV1, j);
+        }
+        const int rv = 2 * n1 - 1;
         wait_full(rv);
-        if (lane == 0) rec(kEvMmaWaitP0, j);
-        issue_pv(0, rv, j > 1, j - 1);
-        wait_full(rk);
-        issue_qk(0, rk);
-        if (lane == 0) rec(kEvMmaIssuedPV0, j);
-        if (lane == 0) rec(kEvMmaWaitP1, j);
-        issue_pv(1, rv, j > 1, j - 1);
+        if (n1 - 1 < n0) issue_pv(0, rv, n1 > 1, n1 - 1);
+        issue_pv(1, rv, n1 > 1, n1 - 1);
         release(rv);
-        issue_qk(1, rk);
-        release(rk);
-        if (lane == 0) rec(kEvMmaIssuedPV1, j);
       }
-      const int rv = 2 * n_kv - 1;
-      wait_full(rv);
-      issue_pv(0, rv, n_kv > 1, n_kv - 1);
-      issue_pv(1, rv, n_kv > 1, n_kv - 1);
-      release(rv);
     }
   }
   } else {
@@ -280,7 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_run = -INFINITY;  // running max used for the exponent (scaled, log2 units)
     float l_run = 0.f;        // running normaliser relative to m_run
 
-    for (int j = 0; j < n_kv; ++j) {
+    const int my_n_kv = n_kv_t[t];
+    for (int j = 0; j < my_n_kv; ++j) {
       mbar_wait(sbar, uint32_t(j & 1));
       tc_fence_after();
       const bool tr = (row == 0);
@@ -298,12 +317,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
 
-      if (j == n_kv - 1) {
-        const int valid = S - j * kBN;  // keys past S were zero-filled by TMA
-        if (valid < kBN) {
+      {
+        // last admitted column of this row in the tile: the ragged tail
+        // (keys >= S, zero-filled by TMA, or >= valid_len[b]) and, on the
+        // causal diagonal tile, key q0 + 128 t + i admitted iff i <= row (q0
+        // is a multiple of the key tile, so the offsets cancel)
+        int lim = kBN - 1;
+        if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
+        if (args.mask == kMaskCausal && j == diag0 + t) lim = min(lim, row);
+        if (lim < kBN - 1) {
 #pragma unroll
           for (int i = 0; i < 128; ++i)
-            if (i >= valid) s[i] = -INFINITY;
+            if (i > lim) s[i] = -INFINITY;
         }
       }
       // row max (8 independent chains)
@@ -401,17 +426,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ------------------------------------------------------------- epilogue
-    mbar_wait(obar, uint32_t((n_kv - 1) & 1));
-    tc_fence_after();
+    // rows with no admitted key (padding valid_len == 0) are exact zeros
+    // with LSE = -inf (finalize, tiled.hpp:231-233); their O was never written
+    if (my_n_kv > 0) {
+      mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
+      tc_fence_after();
+    }
     const int grow = q0 + t * kBM + row;
     const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
     uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t orow[32];
-      tmem_ld32(tO + c * 32, orow);
-      tmem_wait_ld();
-      reg_fence(orow);
+      if (my_n_kv > 0) {
+        tmem_ld32(tO + c * 32, orow);
+        tmem_wait_ld();
+        reg_fence(orow);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) orow[i] = 0u;
+      }
       uint32_t packed[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i)

@@ -9,14 +9,23 @@
 
 namespace ta {
 
+// MaskKind (reference types.hpp:41-76)
+enum FwdMask { kMaskNone = 0, kMaskCausal = 1, kMaskPadding = 2 };
+// key-side padding lengths travel in the kernel parameters (no device copy)
+constexpr int kMaxPaddingBatch = 1024;
+
 struct FwdArgs {
   void* o;           // [BH, S, D] 16-bit, same dtype as inputs
   float* lse;        // [BH, S] fp32 natural-log LSE, or nullptr
   int seq_len;       // S
   float scale_log2;  // softmax scale * log2(e)
+  int mask;          // FwdMask
+  int heads;         // H: batch index of flattened head bh is (bh_offset + bh) / H
+  int bh_offset;     // first flattened head of this launch (chunked host path)
   // diagnostics: when non-null, CTA (0,0) records clock64 timestamps
   // trace[event * kTraceIters + j] for the first kTraceIters K/V iterations
   long long* trace;
+  int valid_len[kMaxPaddingBatch];  // Padding: keys j < valid_len[b] admitted
 };
 
 constexpr int kTraceIters = 64;

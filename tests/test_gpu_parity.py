@@ -29,10 +29,11 @@ def _tdt(dt):
     return {O.F16: torch.float16, O.BF16: torch.bfloat16}[dt]
 
 
-def run_gpu(ta, q, k, v, dt, scale=None, stats=None, causal=False):
+def run_gpu(ta, q, k, v, dt, scale=None, stats=None, causal=False, valid_len=None):
     import torch
     qd, kd, vd = (torch.from_numpy(np.ascontiguousarray(x)).to(_tdt(dt)).cuda() for x in (q, k, v))
-    o, lse = ta.sdpa(qd, kd, vd, causal=causal, scale=scale, return_lse=True, stats=stats)
+    o, lse = ta.sdpa(qd, kd, vd, causal=causal, scale=scale, return_lse=True, stats=stats,
+                     valid_len=valid_len)
     torch.cuda.synchronize()
     return o.double().cpu().numpy(), lse.double().cpu().numpy()
 
@@ -199,3 +200,102 @@ def test_errors_are_loud(ta, cuda_device):
     y = torch.zeros(1, 1, 64, 64, device="cuda", dtype=torch.float32)
     with pytest.raises(ta.UnsupportedScheduleError):
         ta.sdpa(y, y, y)
+
+
+# ------------------------------------------------------------- masks (§8f)
+def _check_lse(lse, want):
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isfinite(lse), fin)
+    assert np.abs(lse[fin] - want[fin]).max(initial=0.0) <= LSE_TOL
+
+
+@pytest.mark.parametrize("dt", [O.F16, O.BF16])
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("S", [1, 32, 130, 255, 256, 257, 512, 700])
+def test_causal_matches_oracle(ta, cuda_device, dt, D, S):
+    # test_tiled.cpp:273-291 (Causal) at the kernel's tile geometry
+    q, k, v = O.make_input((1, 2, S, D), dt, 500 + S)
+    o, lse = run_gpu(ta, q, k, v, dt, causal=True)
+    r = O.sdpa_reference(q, k, v, mask_kind=O.MASK_CAUSAL)
+    assert np.abs(o - r["o"]).max() <= TOL[dt]
+    _check_lse(lse, r["lse"])
+
+
+@pytest.mark.parametrize("dt", [O.F16, O.BF16])
+@pytest.mark.parametrize("D", [64, 128])
+def test_padding_matches_oracle(ta, cuda_device, dt, D):
+    # test_tiled.cpp:359-370 + oracle empty rows: valid_len 0, ragged, full
+    B, H, S = 4, 2, 300
+    vl = [0, 1, 130, 300]
+    q, k, v = O.make_input((B, H, S, D), dt, 61)
+    o, lse = run_gpu(ta, q, k, v, dt, valid_len=vl)
+    r = O.sdpa_reference(q, k, v, mask_kind=O.MASK_PADDING, valid_len=vl)
+    assert not np.any(o[0])  # batch 0: every key masked -> exact zero rows
+    assert np.all(np.isneginf(lse[0]))
+    assert np.abs(o - r["o"]).max() <= TOL[dt]
+    _check_lse(lse, r["lse"])
+
+
+def test_causal_long_sampled_heads(ta, cuda_device):
+    q, k, v = O.make_input((1, 3, 4096, 128), O.BF16, 8)
+    o, lse = run_gpu(ta, q, k, v, O.BF16, causal=True)
+    for h in (0, 2):
+        on, ln = O.sdpa_numpy(q[0, h], k[0, h], v[0, h], causal=True)
+        assert np.abs(o[0, h] - on).max() <= TOL[O.BF16]
+        assert np.abs(lse[0, h] - ln).max() <= LSE_TOL
+
+
+def test_causal_independent_of_future_keys(ta, cuda_device):
+    # test_tiled.cpp:336-357: rows <= i are bitwise independent of K/V rows > i
+    import torch
+    B, H, S, D = 1, 2, 1024, 64
+    q, k, v = (torch.randn(B, H, S, D, device="cuda").half() for _ in range(3))
+    base = ta.sdpa(q, k, v, causal=True)
+    g = torch.Generator().manual_seed(12)
+    for _ in range(5):
+        i = int(torch.randint(0, S - 1, (1,), generator=g))
+        k2, v2 = k.clone(), v.clone()
+        k2[:, :, i + 1:] += 3.5
+        v2[:, :, i + 1:] -= 1.25
+        out = ta.sdpa(q, k2, v2, causal=True)
+        assert torch.equal(out[:, :, : i + 1], base[:, :, : i + 1])
+
+
+def test_causal_row0_is_v0_and_stats(ta, cuda_device):
+    # test_reference.cpp:84-89 and the causal tile-visit formula
+    # (test_tiled.cpp:305-334) at the executed 128x128 tiles
+    st = ta.KernelStats()
+    q, k, v = O.make_input((1, 1, 1000, 64), O.F16, 3)
+    o, _ = run_gpu(ta, q, k, v, O.F16, causal=True, stats=st)
+    assert np.array_equal(o[0, 0, 0], v[0, 0, 0].astype(np.float64))
+    want = sum((min(r0 + 127, 999) + 1 + 127) // 128 for r0 in range(0, 1000, 128))
+    assert st.kv_tiles_visited == want
+
+
+def test_padding_through_chunked_host_entry(ta, cuda_device):
+    # > 64 MB of inputs: the host entry pipelines 16 head chunks, each launch
+    # must map its local heads back to the right batch's valid_len
+    import torch
+    B, H, S, D = 4, 16, 4096, 128
+    vl = [4096, 1000, 0, 2049]
+    g = torch.Generator().manual_seed(3)
+    q, k, v = (torch.randn(B, H, S, D, generator=g).bfloat16() for _ in range(3))
+    o = torch.empty_like(q)
+    ta.sdpa_fwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 0, (B, H, S, D),
+                     ta.BF16, mask_kind=ta.MASK_PADDING, valid_len=vl)
+    dev = ta.sdpa(q.cuda(), k.cuda(), v.cuda(), valid_len=vl).cpu()
+    assert torch.equal(o, dev)
+    assert not torch.any(o[2])
+    for b, h in ((1, 5), (3, 15)):
+        on, _ = O.sdpa_numpy(q[b, h].float().numpy(), k[b, h].float().numpy(),
+                             v[b, h].float().numpy(), valid_len=[vl[b]])
+        assert np.abs(o[b, h].double().numpy() - on[0]).max() <= TOL[O.BF16]
+
+
+def test_causal_host_entry_matches_device(ta, cuda_device):
+    import torch
+    q, k, v = (torch.randn(2, 16, 2048, 128).bfloat16() for _ in range(3))
+    o = torch.empty_like(q)
+    ta.sdpa_fwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 0,
+                     tuple(q.shape), ta.BF16, mask_kind=ta.MASK_CAUSAL)
+    assert torch.equal(o, ta.sdpa(q.cuda(), k.cuda(), v.cuda(), causal=True).cpu())
