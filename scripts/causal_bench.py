@@ -3,10 +3,14 @@ and the causal-effective half of it)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import time
+t_start = time.time()
 import torch
+print(f"[{time.time()-t_start:.1f}s] torch imported", flush=True)
 import paper_2603_01960_b200 as ta
 for (B, H, S, D) in [(8, 32, 4096, 128), (1, 16, 16384, 128), (4, 16, 8192, 64)]:
     q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    print(f"[{time.time()-t_start:.1f}s] inputs B{B} H{H} S{S} D{D}", flush=True)
     for causal in (False, True):
         for _ in range(3):
             ta.sdpa(q, k, v, causal=causal)

@@ -24,6 +24,16 @@ TOL = {O.F16: 5e-3, O.BF16: 2e-2}
 LSE_TOL = 1e-3
 
 
+def oracle_ref(q, k, v, scale=None, mask_kind=O.MASK_NONE, valid_len=None):
+    """C oracle for small S; its BLAS restatement (pinned to it to 1e-12 in
+    tests/test_oracle.py) for larger S so the GPU suite stays fast."""
+    if q.shape[2] < 256:
+        return O.sdpa_reference(q, k, v, scale=scale, mask_kind=mask_kind, valid_len=valid_len)
+    o, lse = O.sdpa_numpy(q, k, v, scale=scale, causal=mask_kind == O.MASK_CAUSAL,
+                          valid_len=valid_len if mask_kind == O.MASK_PADDING else None)
+    return {"o": o, "lse": lse}
+
+
 def _tdt(dt):
     import torch
     return {O.F16: torch.float16, O.BF16: torch.bfloat16}[dt]
@@ -79,7 +89,7 @@ def test_kernel_matches_oracle(ta, cuda_device, dt, D, S):
     B, H = 1, 3
     q, k, v = O.make_input((B, H, S, D), dt, 1000 + S)
     o, lse = run_gpu(ta, q, k, v, dt)
-    r = O.sdpa_reference(q, k, v)
+    r = oracle_ref(q, k, v)
     assert np.abs(o - r["o"]).max() <= TOL[dt]
     assert np.abs(lse - r["lse"]).max() <= LSE_TOL
 
@@ -107,7 +117,7 @@ def test_output_on_dtype_grid_and_matches_snapped_oracle(ta, cuda_device):
 def test_explicit_scale(ta, cuda_device, scale):
     q, k, v = O.make_input((1, 2, 384, 128), O.BF16, 9)
     o, lse = run_gpu(ta, q, k, v, O.BF16, scale=scale)
-    r = O.sdpa_reference(q, k, v, scale=scale)
+    r = oracle_ref(q, k, v, scale=scale)
     assert np.abs(o - r["o"]).max() <= TOL[O.BF16]
     assert np.abs(lse - r["lse"]).max() <= LSE_TOL
 
@@ -117,7 +127,7 @@ def test_large_scores_exercise_lazy_rescale(ta, cuda_device):
     # grows by more than 2^8 across tiles, so the O correction path runs.
     q, k, v = O.make_input((1, 2, 1024, 128), O.F16, 21)
     o, lse = run_gpu(ta, q, k, v, O.F16, scale=1.0)
-    r = O.sdpa_reference(q, k, v, scale=1.0)
+    r = oracle_ref(q, k, v, scale=1.0)
     assert np.abs(o - r["o"]).max() <= 1e-2
     assert np.abs(lse - r["lse"]).max() <= LSE_TOL * 10  # |LSE| ~ 40 here
 
@@ -216,7 +226,7 @@ def test_causal_matches_oracle(ta, cuda_device, dt, D, S):
     # test_tiled.cpp:273-291 (Causal) at the kernel's tile geometry
     q, k, v = O.make_input((1, 2, S, D), dt, 500 + S)
     o, lse = run_gpu(ta, q, k, v, dt, causal=True)
-    r = O.sdpa_reference(q, k, v, mask_kind=O.MASK_CAUSAL)
+    r = oracle_ref(q, k, v, mask_kind=O.MASK_CAUSAL)
     assert np.abs(o - r["o"]).max() <= TOL[dt]
     _check_lse(lse, r["lse"])
 
@@ -229,7 +239,7 @@ def test_padding_matches_oracle(ta, cuda_device, dt, D):
     vl = [0, 1, 130, 300]
     q, k, v = O.make_input((B, H, S, D), dt, 61)
     o, lse = run_gpu(ta, q, k, v, dt, valid_len=vl)
-    r = O.sdpa_reference(q, k, v, mask_kind=O.MASK_PADDING, valid_len=vl)
+    r = oracle_ref(q, k, v, mask_kind=O.MASK_PADDING, valid_len=vl)
     assert not np.any(o[0])  # batch 0: every key masked -> exact zero rows
     assert np.all(np.isneginf(lse[0]))
     assert np.abs(o - r["o"]).max() <= TOL[dt]
@@ -289,7 +299,7 @@ def test_padding_through_chunked_host_entry(ta, cuda_device):
     for b, h in ((1, 5), (3, 15)):
         on, _ = O.sdpa_numpy(q[b, h].float().numpy(), k[b, h].float().numpy(),
                              v[b, h].float().numpy(), valid_len=[vl[b]])
-        assert np.abs(o[b, h].double().numpy() - on[0]).max() <= TOL[O.BF16]
+        assert np.abs(o[b, h].double().numpy() - on).max() <= TOL[O.BF16]
 
 
 def test_causal_host_entry_matches_device(ta, cuda_device):
