@@ -198,10 +198,10 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_2603_01960_b200.sharding import head_range, max_over_ranks
     B, H, S, D = WORKLOAD["B"], WORKLOAD["H"], WORKLOAD["S"], WORKLOAD["D"]
-    if H % world:
-        raise SystemExit(f"H={H} not divisible by {world} GPUs")
-    Hl = H // world  # head sharding: this rank owns heads [rank*Hl, (rank+1)*Hl)
+    h0, h1 = head_range(H, world, rank)  # head sharding: this rank owns heads [h0, h1)
+    Hl = h1 - h0
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     q, k, v = (torch.randn(B, Hl, S, D, device=dev, generator=g, dtype=torch.bfloat16)
                for _ in range(3))
@@ -239,9 +239,7 @@ def run_ours(args):
     total_ms = t_start.elapsed_time(t_end)
     per_launch = [e0.elapsed_time(e1) for e0, e1 in evs]
     if world > 1:
-        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = tt.item()
+        total_ms = max_over_ranks(total_ms, device=dev)
     ms_step = total_ms / args.steps
     job_flops = flops(B, H, S, D)
     value = job_flops / (ms_step / 1e3) / 1e12
@@ -287,9 +285,7 @@ def run_ours(args):
         barrier()
         e2e_s = (time.perf_counter() - t0) / n_e2e
         if world > 1:
-            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = tt.item()
+            e2e_s = max_over_ranks(e2e_s, device=dev)
         nbytes = q.numel() * 2
         e2e = {"value": job_flops / e2e_s / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": 3 * nbytes * world, "d2h_bytes_per_step": nbytes * world,
