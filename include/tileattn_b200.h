@@ -113,6 +113,14 @@ TA_API ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, v
                            const int64_t* valid_len, int has_scale, double scale,
                            ta_schedule sched, void* stream, ta_kernel_stats* stats);
 
+/* Validation only: the status ta_sdpa_fwd / ta_sdpa_fwd_host would return for
+ * these arguments before touching any device (reference order shape -> mask ->
+ * schedule -> scale, then what the sm_100a kernel covers).  Lets a harness
+ * record status=unsupported rows (bench.cpp:290-292) without allocating. */
+TA_API ta_status ta_sdpa_check(ta_shape shape, ta_dtype dtype, ta_mask_kind mask,
+                               const int64_t* valid_len, int has_scale, double scale,
+                               ta_schedule sched);
+
 /* Thread-local message for the last non-OK status (exception what()). */
 TA_API const char* ta_last_error(void);
 

@@ -124,6 +124,8 @@ def lib() -> ctypes.CDLL:
     L.ta_plan_cache_clear.restype = None
     L.ta_device_supported.restype = cint
     L.ta_device_supported.argtypes = [cint]
+    L.ta_sdpa_check.restype = cint
+    L.ta_sdpa_check.argtypes = [_Shape, cint, cint, vp, cint, dbl, _Schedule]
     L.ta_debug_umma_gemm.restype = cint
     L.ta_debug_umma_gemm.argtypes = [cint, cint, vp, vp, vp, vp]
     _lib = L

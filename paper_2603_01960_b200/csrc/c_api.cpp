@@ -350,6 +350,16 @@ void ta_plan_cache_clear(void) {
   c.constructions = 0;
 }
 
+ta_status ta_sdpa_check(ta_shape shape, ta_dtype dtype, ta_mask_kind mask,
+                        const int64_t* valid_len, int has_scale, double scale,
+                        ta_schedule sched) {
+  sched = resolve_schedule(sched);
+  double eff = 0.0;
+  ta_status st = validate_common(shape, mask, valid_len, sched, has_scale, scale, &eff);
+  if (st != TA_OK) return st;
+  return validate_device_support(shape, dtype, mask);
+}
+
 int ta_device_supported(int device) { return device_cc(device) == 100 ? 1 : 0; }
 
 ta_status ta_sdpa_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
