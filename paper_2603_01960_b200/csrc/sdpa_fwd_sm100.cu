@@ -471,6 +471,358 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ----------------------------------------------------------------------------
+// Variant "db": one 128-row Q tile per CTA with double-buffered S in TMEM.
+// The tensor core computes S(j+1) while the softmax of S(j) runs and then
+// PV(j); the softmax runs back to back against a 1024-cycle MMA budget per
+// K/V tile (D=128) instead of racing the other Q tile of a ping-pong pair.
+// ----------------------------------------------------------------------------
+constexpr int kThreadsDB = 256;  // warps 0-3 softmax, 4 TMEM alloc, 5 TMA, 7 MMA
+constexpr int kDBWarpAlloc = 4, kDBWarpTma = 5, kDBWarpMma = 7;
+
+template <int D>
+struct CfgDB {
+  static constexpr int kRegions = D / 64;
+  static constexpr int kTileBytes = kBM * D * 2;
+  static constexpr int kRegionBytes = kBM * 128;
+  static constexpr int kSlots = D == 128 ? 6 : 12;
+  static constexpr int kSmemData = kTileBytes + kSlots * kTileBytes;
+  static constexpr int kSmemBytes = kSmemData + 1024 + 1024;
+  static constexpr uint32_t kTmemS = 0;    // S buffers at cols 0 and 128
+  static constexpr uint32_t kTmemO = 256;  // O at 256 .. 256 + D
+};
+
+struct BarriersDB {
+  uint64_t q_full;
+  uint64_t s_full[2];   // per S buffer
+  uint64_t p_full[2];   // P halves (keys [0,64) / [64,128)) of the current tile
+  uint64_t o_full;      // PV(j) complete
+  uint64_t slot_full[12];
+  uint64_t slot_empty[12];
+  uint32_t tmem_base;
+};
+
+template <int D, bool kBF16>
+__global__ void __launch_bounds__(kThreadsDB, 1)
+    sdpa_fwd_db_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                       const __grid_constant__ CUtensorMap tmap_k,
+                       const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
+  using C = CfgDB<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sq = smem_u32(smem);
+  const uint32_t sring = sq + C::kTileBytes;
+  BarriersDB* bars = reinterpret_cast<BarriersDB*>(smem + C::kSmemData);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int S = args.seq_len;
+  const int bh = blockIdx.y;
+  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
+  const int q0 = qblk * kBM;
+  const int kv_len =
+      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
+  const int n_kv_seq = (kv_len + kBN - 1) / kBN;
+  const int diag = q0 / kBN;  // causal: the K/V tile on this Q tile's diagonal
+  const int n_kv = args.mask == kMaskCausal ? min(diag + 1, n_kv_seq) : n_kv_seq;
+  long long* const trace =
+      (args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+  auto rec = [&](int ev, int j) {
+    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
+  };
+  // K/V ring order = MMA consumption order: K0, K1, V0, K2, V1, K3, V2, ...
+  // (S(j+2) is issued right after PV(j)).
+
+  if (threadIdx.x == kDBWarpTma * 32) {
+    mbar_init(smem_u32(&bars->q_full), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&bars->s_full[b]), 1);
+      mbar_init(smem_u32(&bars->p_full[b]), kBM / 32);
+    }
+    mbar_init(smem_u32(&bars->o_full), 1);
+    for (int s = 0; s < C::kSlots; ++s) {
+      mbar_init(smem_u32(&bars->slot_full[s]), 1);
+      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kDBWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  // the consumption sequence as (tile, is_v) pairs, generated in order:
+  // K0, [K1], then for i = 0..n-1: V_i, [K_{i+2}]
+  if (warp == kDBWarpTma) {
+    // ------------------------------------------------------------------ TMA
+    if (lane == 0 && n_kv > 0) {
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+      const uint32_t qbar = smem_u32(&bars->q_full);
+      mbar_arrive_expect_tx(qbar, C::kTileBytes);
+      for (int r = 0; r < C::kRegions; ++r)
+        tma_load_3d(sq + r * C::kRegionBytes, &tmap_q, qbar, r * 64, q0, bh);
+      int slot = 0;
+      uint32_t phase = 0;
+      auto load = [&](const CUtensorMap* map, int tile) {
+        mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
+        const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+        mbar_arrive_expect_tx(fbar, C::kTileBytes);
+        for (int r = 0; r < C::kRegions; ++r)
+          tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
+                      tile * kBN, bh);
+        if (++slot == C::kSlots) {
+          slot = 0;
+          phase ^= 1;
+        }
+      };
+      load(&tmap_k, 0);
+      if (n_kv > 1) load(&tmap_k, 1);
+      for (int i = 0; i < n_kv; ++i) {
+        load(&tmap_v, i);
+        if (i + 2 < n_kv) load(&tmap_k, i + 2);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kDBWarpMma) {
+    // ------------------------------------------------------------------ MMA
+    constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
+    constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+    int pos = 0;  // position in the ring sequence
+    auto slot_of = [](int r) { return r % C::kSlots; };
+    auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
+    auto wait_full = [&](int r) {
+      mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
+      tc_fence_after();
+    };
+    auto release = [&](int r) { umma_commit_warp(smem_u32(&bars->slot_empty[slot_of(r)])); };
+    const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
+    const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
+    const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
+    auto issue_qk = [&](int buf, int r) {
+      uint64_t qd = qdesc;
+      uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+      asm volatile("" : "+l"(qd), "+l"(kd));
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
+        umma_ss_warp(tmem + C::kTmemS + buf * kBN, qd + off, kd + off, idesc_qk, ks > 0);
+      }
+      umma_commit_warp(smem_u32(&bars->s_full[buf]));
+    };
+    auto issue_pv = [&](int buf, int r, bool accumulate, int j) {
+      uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+      asm volatile("" : "+l"(vd));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        mbar_wait(smem_u32(&bars->p_full[h]), uint32_t(j & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBN / 32; ++kk) {
+          const int ks = h * (kBN / 32) + kk;
+          umma_ts_warp(tmem + C::kTmemO, tmem + C::kTmemS + buf * kBN + ks * 8,
+                       vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+                       (accumulate || ks > 0) ? 1u : 0u);
+        }
+      }
+      umma_commit_warp(smem_u32(&bars->o_full));
+    };
+    if (n_kv > 0) {
+      mbar_wait(smem_u32(&bars->q_full), 0);
+      tc_fence_after();
+      wait_full(pos);
+      issue_qk(0, pos);
+      release(pos++);
+      if (n_kv > 1) {
+        wait_full(pos);
+        issue_qk(1, pos);
+        release(pos++);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        wait_full(pos);
+        if (lane == 0) rec(kEvMmaWaitP0, j);
+        issue_pv(j & 1, pos, j > 0, j);
+        release(pos++);
+        if (lane == 0) rec(kEvMmaIssuedPV0, j);
+        if (j + 2 < n_kv) {
+          wait_full(pos);
+          issue_qk(j & 1, pos);  // S(j+2) reuses the buffer PV(j) just read
+          release(pos++);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // -------------------------------------------------------------- softmax
+    const uint32_t wq = warp & 3;
+    const int row = int(wq * 32 + lane);
+    const uint32_t lane_off = (wq * 32u) << 16;
+    const uint32_t tO = tmem + lane_off + C::kTmemO;
+    const float sl2 = args.scale_log2;
+    const uint32_t obar = smem_u32(&bars->o_full);
+    float m_run = -INFINITY;
+    float l_run = 0.f;
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    const bool tr = (row == 0);
+
+    for (int j = 0; j < n_kv; ++j) {
+      const int buf = j & 1;
+      const uint32_t tS = tmem + lane_off + C::kTmemS + buf * kBN;
+      mbar_wait(smem_u32(&bars->s_full[buf]), uint32_t((j >> 1) & 1));
+      tc_fence_after();
+      if (tr) rec(kEvSm0SReady, j);
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
+      if (tr) rec(kEvSm0Loaded, j);
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
+      {
+        int lim = kBN - 1;
+        if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
+        if (args.mask == kMaskCausal && j == diag) lim = min(lim, row);
+        if (lim < kBN - 1) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i > lim) s[i] = -INFINITY;
+        }
+      }
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+#pragma unroll
+      for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float m_new = mx * sl2;
+      if (tr) rec(kEvSm0Max, j);
+      const bool need = m_new > m_run + kRescaleThreshold;
+      const float alpha = need ? ex2(m_run - m_new) : 1.f;
+      if (need) {
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // O holds PV(0..j-1); wait for PV(j-1), rescale in place (PV(j) waits
+        // for P(j), signalled below)
+        mbar_wait(obar, uint32_t((j - 1) & 1));
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orow[32];
+          tmem_ld32(tO + c * 32, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+          tmem_st32(tO + c * 32, orow);
+        }
+      }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      const uint64_t negm2 = f2(-m_use, -m_use);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const int c0 = h * 64 + g * 8;
+          uint64_t x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
+          float p[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#ifdef TA_DEBUG_NO_EXP
+            if (true) {
+              f2_split(x[u], p[2 * u], p[2 * u + 1]);
+            } else
+#endif
+            if (2 * u >= 8 - kEmuPer8) {
+              ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
+            } else {
+              float a, b;
+              f2_split(x[u], a, b);
+              p[2 * u] = ex2(a);
+              p[2 * u + 1] = ex2(b);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
+            pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+          }
+        }
+        tmem_st32(tS + h * 32, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[h]));
+        if (h == 0 && tr) rec(kEvSm0Exp, j);
+      }
+      {
+        const uint64_t a01 = fadd2(acc[0], acc[1]);
+        const uint64_t a23 = fadd2(acc[2], acc[3]);
+        float lo, hi;
+        f2_split(fadd2(a01, a23), lo, hi);
+        l_run += lo + hi;
+      }
+      if (tr) rec(kEvSm0PArrive, j);
+    }
+
+    // ------------------------------------------------------------- epilogue
+    if (n_kv > 0) {
+      mbar_wait(obar, uint32_t((n_kv - 1) & 1));
+      tc_fence_after();
+    }
+    const int grow = q0 + row;
+    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t orow[32];
+      if (n_kv > 0) {
+        tmem_ld32(tO + c * 32, orow);
+        tmem_wait_ld();
+        reg_fence(orow);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) orow[i] = 0u;
+      }
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
+                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
+      if (grow < S) {
+        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                              packed[4 * i + 3]);
+      }
+    }
+    if (args.lse != nullptr && grow < S)
+      args.lse[size_t(bh) * S + grow] =
+          l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kDBWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
+}
+
+// ----------------------------------------------------------------------------
 // Descriptor self-test: one 128x128x128 UMMA product, checked on the host.
 //   mode 0: D = A * B^T, A [128][128] K-major, B [128 n][128 k] K-major (QK^T)
 //   mode 1: D = A * B,   A K-major, B [128 k][128 n] MN-major       (PV, SS)
@@ -559,7 +911,27 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 template <int D, bool kBF16>
+cudaError_t launch_db(const FwdLaunch& L) {
+  using C = CfgDB<D>;
+  auto kern = sdpa_fwd_db_kernel<D, kBF16>;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  dim3 grid((L.args.seq_len + kBM - 1) / kBM, L.bh);
+  kern<<<grid, kThreadsDB, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
+  return cudaGetLastError();
+}
+
+template <int D, bool kBF16>
 cudaError_t launch_typed(const FwdLaunch& L) {
+  if (L.variant == 1) return launch_db<D, kBF16>(L);
   using C = Cfg<D>;
   auto kern = sdpa_fwd_kernel<D, kBF16>;
   static bool attr_set[64] = {};  // per device
@@ -580,17 +952,20 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 
 }  // namespace
 
-FwdGeometry fwd_geometry(int64_t S, int64_t BH) {
+FwdGeometry fwd_geometry(int64_t S, int64_t BH, int variant) {
   FwdGeometry g;
   g.block_m = kBM;
   g.block_n = kBN;
-  g.q_tiles_per_cta = kQTiles;
-  g.threads = kThreads;
-  g.ctas = ((S + kBM * kQTiles - 1) / (kBM * kQTiles)) * BH;
+  g.q_tiles_per_cta = variant == 1 ? 1 : kQTiles;
+  g.threads = variant == 1 ? kThreadsDB : kThreads;
+  g.ctas = ((S + kBM * g.q_tiles_per_cta - 1) / (kBM * g.q_tiles_per_cta)) * BH;
   return g;
 }
 
-int fwd_ring_slots(int D) { return D == 128 ? Cfg<128>::kSlots : Cfg<64>::kSlots; }
+int fwd_ring_slots(int D, int variant) {
+  if (variant == 1) return D == 128 ? CfgDB<128>::kSlots : CfgDB<64>::kSlots;
+  return D == 128 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
+}
 
 cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
   if (L.head_dim == 128) return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
