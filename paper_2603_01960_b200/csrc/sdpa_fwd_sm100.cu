@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 
 #include "ptx_sm100.cuh"
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int h = 0; h < kPParts; ++h) {
           mbar_wait(smem_u32(&bars->p_full[t][h]), uint32_t(j & 1));
           tc_fence_after();
+          if (h == kPParts - 1 && lane == 0) rec(t == 0 ? kEvMmaWaitP0 : kEvMmaWaitP1, j);
 #pragma unroll
           for (int kk = 0; kk < kBN / 16 / kPParts; ++kk) {
             const int ks = h * (kBN / 16 / kPParts) + kk;
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit_warp(smem_u32(&bars->o_full[t]));
+        if (lane == 0) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
       };
 
       // Q tile 0 visits n0 <= n1 K/V tiles (fewer under the causal mask)
@@ -262,17 +265,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 1; j < n1; ++j) {
           const int rk = 2 * j, rv = 2 * j - 1;
           wait_full(rv);
-          if (lane == 0) rec(kEvMmaWaitP0, j);
           if (j - 1 < n0) issue_pv(0, rv, j > 1, j - 1);
           wait_full(rk);
           if (j < n0) issue_qk(0, rk);
-          if (lane == 0) rec(kEvMmaIssuedPV0, j);
-          if (lane == 0) rec(kEvMmaWaitP1, j);
           issue_pv(1, rv, j > 1, j - 1);
           release(rv);
           issue_qk(1, rk);
           release(rk);
-          if (lane == 0) rec(kEvMmaIssuedPV1, j);
         }
         const int rv = 2 * n1 - 1;
         wait_full(rv);
@@ -468,6 +467,1108 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == kWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
+}
+
+// ----------------------------------------------------------------------------
+// Variant "rs" (row split): the ping-pong kernel above with 16 softmax warps,
+// two per TMEM lane quadrant per Q tile.  Warp w (t = w / 8, rh = (w / 4) & 1,
+// quadrant q = w & 3) owns rows q*32 + rh*16 + [0, 16); with the 16x32bx2
+// TMEM shape lane l holds row (l & 15) and key half l >> 4 (64 columns), so a
+// row's max / sum is one xor-16 shuffle.  Each SMSP then runs two softmax
+// warps per Q tile: the latency of one tile's softmax is about halved, which
+// is what the 2-tile ping-pong needs (softmax(t) must fit under the MMAs of
+// the other tile, ~1024 cycles at D=128).
+// ----------------------------------------------------------------------------
+constexpr int kThreadsRS = 640;  // 20 warps: 16 softmax + TMEM alloc, TMA, spare, MMA
+constexpr int kRSWarpAlloc = 16, kRSWarpTma = 17, kRSWarpMma = 19;
+// Registers are allocated per SMSP (warp w lives on SMSP w % 4): 5 warps per
+// SMSP cap the launch allocation at 96; setmaxnreg moves 64 from each control
+// thread to the softmax threads (4 x 32 x 112 + 32 x 32 = 15360 <= 16384).
+constexpr int kRSLaunchRegs = 96;
+constexpr int kRSRegsControl = 32;
+constexpr int kRSRegsSoftmax = 112;
+static_assert(16 * 32 * (kRSRegsSoftmax - kRSLaunchRegs) <=
+                  4 * 32 * (kRSLaunchRegs - kRSRegsControl),
+              "setmaxnreg.inc would wait forever: register pool does not balance");
+
+template <int D, bool kBF16, bool kTrace>
+__global__ void __launch_bounds__(kThreadsRS, 1)
+    sdpa_fwd_rs_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                       const __grid_constant__ CUtensorMap tmap_k,
+                       const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sq = smem_u32(smem);
+  const uint32_t sring = sq + kQTiles * C::kTileBytes;
+  Barriers* bars = reinterpret_cast<Barriers*>(smem + C::kSmemData);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int S = args.seq_len;
+  const int bh = blockIdx.y;
+  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
+  const int q0 = qblk * (kBM * kQTiles);
+  const int kv_len =
+      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
+  const int n_kv_seq = (kv_len + kBN - 1) / kBN;
+  const int diag0 = q0 / kBN;
+  int n_kv_t[kQTiles];
+#pragma unroll
+  for (int t = 0; t < kQTiles; ++t)
+    n_kv_t[t] = args.mask == kMaskCausal ? min(diag0 + t + 1, n_kv_seq) : n_kv_seq;
+  const int n_kv = n_kv_t[kQTiles - 1];
+  long long* const trace =
+      (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+  auto rec = [&](int ev, int j) {
+    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
+  };
+
+  if (threadIdx.x == kRSWarpMma * 32) {
+    mbar_init(smem_u32(&bars->q_full), 1);
+    for (int t = 0; t < kQTiles; ++t) {
+      mbar_init(smem_u32(&bars->s_full[t]), 1);
+      for (int q = 0; q < 2; ++q) mbar_init(smem_u32(&bars->p_full[t][q]), 8);  // 8 warps/tile
+      mbar_init(smem_u32(&bars->o_full[t]), 1);
+    }
+    for (int s = 0; s < C::kSlots; ++s) {
+      mbar_init(smem_u32(&bars->slot_full[s]), 1);
+      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kRSWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp >= 16) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRSRegsControl));
+  if (warp == kRSWarpTma) {
+    // ------------------------------------------------------------------ TMA
+    if (lane == 0) {
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+      const uint32_t qbar = smem_u32(&bars->q_full);
+      if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
+      for (int t = 0; t < kQTiles && n_kv > 0; ++t)
+        for (int r = 0; r < C::kRegions; ++r)
+          tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
+                      q0 + t * kBM, bh);
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n_kv; ++j) {
+        for (int kv = 0; kv < 2; ++kv) {
+          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
+          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+          mbar_arrive_expect_tx(fbar, C::kTileBytes);
+          const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
+          for (int r = 0; r < C::kRegions; ++r)
+            tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
+                        j * kBN, bh);
+          if (++slot == C::kSlots) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kRSWarpMma) {
+    // ------------------------------------------------------------------ MMA
+    // Register-lean (32 registers after setmaxnreg): barrier addresses are
+    // re-derived from an opaque base at each use instead of being hoisted.
+    constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
+    constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+    const uint32_t bb = smem_u32(bars);
+    auto bar = [&](uint32_t off) { return opaque(bb) + off; };
+    auto slot_of = [](int r) { return r % C::kSlots; };
+    auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
+    auto wait_full = [&](int r) {
+      mbar_wait(bar(offsetof(Barriers, slot_full) + 8 * slot_of(r)), phase_of(r));
+      tc_fence_after();
+    };
+    auto release = [&](int r) {
+      umma_commit_warp(bar(offsetof(Barriers, slot_empty) + 8 * slot_of(r)));
+    };
+    const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
+    const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
+    const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
+    auto issue_qk = [&](int t, int r) {
+      uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
+      uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+      asm volatile("" : "+l"(qd), "+l"(kd));
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
+        umma_ss_warp(opaque(tmem) + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
+      }
+      umma_commit_warp(bar(offsetof(Barriers, s_full) + 8 * t));
+    };
+    // P of key k sits in packed column k / 2; part h = K-steps {2h, 2h+1,
+    // 4+2h, 5+2h} (keys [32h, 32h+32) of each key half of the rows).
+    auto issue_pv = [&](int t, int r, bool accumulate, int j) {
+      uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+      asm volatile("" : "+l"(vd));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        mbar_wait(bar(offsetof(Barriers, p_full) + 8 * (4 * t + h)), uint32_t(j & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int ks = (kk >> 1) * 4 + 2 * h + (kk & 1);
+          umma_ts_warp(opaque(tmem) + C::kTmemO + t * D, opaque(tmem) + C::kTmemS + t * kBN + ks * 8,
+                       vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+                       (accumulate || h > 0 || kk > 0) ? 1u : 0u);
+        }
+      }
+      umma_commit_warp(bar(offsetof(Barriers, o_full) + 8 * t));
+    };
+    const int n0 = n_kv_t[0], n1 = n_kv_t[1];
+    if (n1 > 0) {
+      mbar_wait(smem_u32(&bars->q_full), 0);
+      tc_fence_after();
+      wait_full(0);
+      if (n0 > 0) issue_qk(0, 0);
+      issue_qk(1, 0);
+      release(0);
+      for (int j = 1; j < n1; ++j) {
+        const int rk = 2 * j, rv = 2 * j - 1;
+        wait_full(rv);
+        if (j - 1 < n0) issue_pv(0, rv, j > 1, j - 1);
+        wait_full(rk);
+        if (j < n0) issue_qk(0, rk);
+        issue_pv(1, rv, j > 1, j - 1);
+        release(rv);
+        issue_qk(1, rk);
+        release(rk);
+      }
+      const int rv = 2 * n1 - 1;
+      wait_full(rv);
+      if (n1 - 1 < n0) issue_pv(0, rv, n1 > 1, n1 - 1);
+      issue_pv(1, rv, n1 > 1, n1 - 1);
+      release(rv);
+    }
+  }
+  } else {
+    // -------------------------------------------------------------- softmax
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRSRegsSoftmax));
+    const int t = int(warp) >> 3;
+    const int wq = int(warp) & 3;
+    const int rh = (int(warp) >> 2) & 1;
+    const int hl = int(lane) >> 4;                        // key half of the row
+    const int row = wq * 32 + rh * 16 + (int(lane) & 15);  // row in the Q tile
+    const uint32_t lane_off = uint32_t(wq * 32 + rh * 16) << 16;
+    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN;
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
+    constexpr int kOHalf = D / 2;  // O columns per thread
+    const float sl2 = args.scale_log2;
+    const uint32_t sbar = smem_u32(&bars->s_full[t]);
+    const uint32_t obar = smem_u32(&bars->o_full[t]);
+    const bool tr = kTrace && trace != nullptr && (warp & 7) == 0 && lane == 0;
+    const int key0 = hl * 64;  // first key of my column half
+
+    float m_run = -INFINITY;  // running max (scaled, log2 units), same in both halves
+    float l_run = 0.f;        // my half's partial normaliser relative to m_run
+
+    // P layout: the 16-bit P of my key half goes to packed columns
+    // [32 hl, 32 hl + 32) of the S tile (key k -> column k / 2); both halves
+    // of a row are read (tcgen05.wait::ld) before either writes.  P is handed
+    // to the MMA in two parts: part h = keys [32h, 32h+32) + [64+32h, 96+32h).
+    const int my_n_kv = n_kv_t[t];
+    for (int j = 0; j < my_n_kv; ++j) {
+      mbar_wait(sbar, uint32_t(j & 1));
+      tc_fence_after();
+      if (tr) rec(kEvSm0SReady + 5 * t, j);
+      uint32_t sr[2][32];
+      tmem_ld_16x32bx2_x32<64>(tS, sr[0]);
+      tmem_ld_16x32bx2_x32<64>(tS + 32, sr[1]);
+      int lim = kBN - 1;
+      if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
+      if (args.mask == kMaskCausal && j == diag0 + t) lim = min(lim, row);
+      const int llim = lim - key0;  // last admitted local column
+      tmem_wait_ld();
+      reg_fence(sr[0]);
+      reg_fence(sr[1]);
+      float s[64];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
+      if (__any_sync(0xffffffffu, llim < 63)) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i > llim) s[i] = -INFINITY;
+      }
+      if (tr) rec(kEvSm0Loaded + 5 * t, j);
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+#pragma unroll
+      for (int i = 8; i < 64; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const float m_new = mx * sl2;
+      if (tr) rec(kEvSm0Max + 5 * t, j);
+      const bool need = m_new > m_run + kRescaleThreshold;
+      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
+      if (need) {
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // O holds PV(0..j-1): wait for PV(j-1), rescale in place (PV(j)
+        // waits for P(j), signalled below)
+        mbar_wait(obar, uint32_t((j - 1) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kOHalf / 16; ++c) {
+          uint32_t orow[16];
+          tmem_ld_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+          tmem_st_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
+        }
+      }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      const uint64_t sl2x2 = f2(sl2, sl2);
+      const uint64_t negm2 = f2(-m_use, -m_use);
+      uint64_t acc[2] = {0ull, 0ull};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {  // 16 columns -> 8 packed P words
+          uint32_t pk[8];
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {  // groups of 8 columns
+            const int c0 = h * 32 + qq * 16 + g * 8;
+            uint64_t x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
+            float p[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+#ifdef TA_DEBUG_NO_EXP
+              if (true) {
+                f2_split(x[u], p[2 * u], p[2 * u + 1]);
+              } else
+#endif
+              if (2 * u >= 8 - kEmuPer8) {
+                ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
+              } else {
+                float a, b2;
+                f2_split(x[u], a, b2);
+                p[2 * u] = ex2(a);
+                p[2 * u + 1] = ex2(b2);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              acc[u & 1] = fadd2(acc[u & 1], f2(p[2 * u], p[2 * u + 1]));
+              pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+            }
+          }
+          // keys key0 + 32h + 16qq + [0, 16) -> packed columns 32 hl + 16h + 8qq + [0, 8)
+          tmem_st_16x32bx2_x8<32>(tS + h * 16 + qq * 8, pk);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
+        if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
+      }
+      {
+        float lo, hi;
+        f2_split(fadd2(acc[0], acc[1]), lo, hi);
+        l_run += lo + hi;
+      }
+      if (tr) rec(kEvSm0PArrive + 5 * t, j);
+    }
+
+    // ------------------------------------------------------------- epilogue
+    if (my_n_kv > 0) {
+      mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
+      tc_fence_after();
+    }
+    const float l_row = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
+    const int grow = q0 + t * kBM + row;
+    const float inv_l = l_row > 0.f ? 1.f / l_row : 0.f;
+    uint16_t* orow_g =
+        reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D + hl * kOHalf;
+#pragma unroll
+    for (int c = 0; c < kOHalf / 32; ++c) {
+      uint32_t orow[32];
+      if (my_n_kv > 0) {
+        tmem_ld_16x32bx2_x32<kOHalf>(tO + c * 32, orow);
+        tmem_wait_ld();
+        reg_fence(orow);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) orow[i] = 0u;
+      }
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
+                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
+      if (grow < S) {
+        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                              packed[4 * i + 3]);
+      }
+    }
+    if (args.lse != nullptr && grow < S && hl == 0)
+      args.lse[size_t(bh) * S + grow] =
+          l_row > 0.f ? (m_run + __log2f(l_row)) * kLn2 : -INFINITY;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kRSWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
+}
+
+// ----------------------------------------------------------------------------
+// Variant "x" (default): 64-key K/V tiles with double-buffered S per Q tile.
+// TMEM: S(t, b) at columns 128 t + 64 b (fp32, P written over it in 16-bit),
+// O(t) at 256 + D t.  The tensor core computes S(j+1) of both Q tiles while
+// the softmax of S(j) runs, so the softmax's TMEM-read latency and its exps
+// are no longer in series with the MMA round trip: the loop runs at
+// max(tensor time, softmax throughput) instead of their sum.  16 softmax
+// warps as in "rs" (two threads per row, 32 keys each per tile).
+// MMA issue order: S0(0) S1(0) | S0(1) S1(1) PV0(0) PV1(0) | S0(2) S1(2) PV0(1)..
+// (S_t(j+2) reuses the buffer PV_t(j) has read: in-order tensor pipe).
+// ----------------------------------------------------------------------------
+constexpr int kBNX = 64;         // keys per K/V tile
+constexpr int kThreadsX = 640;   // 20 warps: 16 softmax + TMEM alloc, TMA, spare, MMA
+constexpr int kXWarpAlloc = 16, kXWarpTma = 17, kXWarpMma = 19;
+constexpr int kXRegsControl = 56;
+constexpr int kXRegsSoftmax = 104;
+static_assert(16 * 32 * (kXRegsSoftmax - kRSLaunchRegs) <= 4 * 32 * (kRSLaunchRegs - kXRegsControl),
+              "setmaxnreg.inc would wait forever: register pool does not balance");
+
+template <int D>
+struct CfgX {
+  static constexpr int kRegions = D / 64;
+  static constexpr int kQTileBytes = kBM * D * 2;
+  static constexpr int kQRegionBytes = kBM * 128;
+  static constexpr int kKVTileBytes = kBNX * D * 2;
+  static constexpr int kKVRegionBytes = kBNX * 128;
+  static constexpr int kSlots = D == 128 ? 8 : 16;
+  static constexpr int kSmemData = kQTiles * kQTileBytes + kSlots * kKVTileBytes;
+  static constexpr int kSmemBytes = kSmemData + 1024 + 1024;
+  static constexpr uint32_t kTmemO = 256;
+};
+
+struct BarriersX {
+  uint64_t q_full;
+  uint64_t s_full[kQTiles][2];  // [tile][S buffer]
+  uint64_t p_full[kQTiles];     // P_t(j) written (8 warp arrivals)
+  uint64_t o_full[kQTiles];     // PV_t(j) complete
+  uint64_t slot_full[16];
+  uint64_t slot_empty[16];
+  uint32_t tmem_base;
+};
+
+template <int D, bool kBF16, bool kTrace>
+__global__ void __launch_bounds__(kThreadsX, 1)
+    sdpa_fwd_x_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                      const __grid_constant__ CUtensorMap tmap_k,
+                      const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
+  using C = CfgX<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sq = smem_u32(smem);
+  const uint32_t sring = sq + kQTiles * C::kQTileBytes;
+  BarriersX* bars = reinterpret_cast<BarriersX*>(smem + C::kSmemData);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int S = args.seq_len;
+  const int bh = blockIdx.y;
+  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
+  const int q0 = qblk * (kBM * kQTiles);
+  const int kv_len =
+      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
+  const int n_kv_seq = (kv_len + kBNX - 1) / kBNX;
+  // trip counts (causal: kv_end = last_row / t_n + 1, tiled.cpp:159)
+  const int n0 = args.mask == kMaskCausal ? min((q0 + kBM - 1) / kBNX + 1, n_kv_seq) : n_kv_seq;
+  const int n1 =
+      args.mask == kMaskCausal ? min((q0 + 2 * kBM - 1) / kBNX + 1, n_kv_seq) : n_kv_seq;
+  long long* const trace = (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+  auto rec = [&](int ev, int j) {
+    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
+  };
+
+  if (threadIdx.x == kXWarpMma * 32) {
+    mbar_init(smem_u32(&bars->q_full), 1);
+    for (int t = 0; t < kQTiles; ++t) {
+      mbar_init(smem_u32(&bars->s_full[t][0]), 1);
+      mbar_init(smem_u32(&bars->s_full[t][1]), 1);
+      mbar_init(smem_u32(&bars->p_full[t]), 8);
+      mbar_init(smem_u32(&bars->o_full[t]), 1);
+    }
+    for (int s = 0; s < C::kSlots; ++s) {
+      mbar_init(smem_u32(&bars->slot_full[s]), 1);
+      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kXWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp >= 16) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kXRegsControl));
+    if (warp == kXWarpTma) {
+      // ---------------------------------------------------------------- TMA
+      // ring order = MMA consumption order: K0 | K1 V0 | K2 V1 | ... | V(n-1)
+      if (lane == 0 && n1 > 0) {
+        tma_prefetch_desc(&tmap_q);
+        tma_prefetch_desc(&tmap_k);
+        tma_prefetch_desc(&tmap_v);
+        const uint32_t qbar = smem_u32(&bars->q_full);
+        mbar_arrive_expect_tx(qbar, kQTiles * C::kQTileBytes);
+        for (int t = 0; t < kQTiles; ++t)
+          for (int r = 0; r < C::kRegions; ++r)
+            tma_load_3d(sq + t * C::kQTileBytes + r * C::kQRegionBytes, &tmap_q, qbar, r * 64,
+                        q0 + t * kBM, bh);
+        int slot = 0;
+        uint32_t phase = 0;
+        auto load = [&](const CUtensorMap* map, int tile) {
+          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
+          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+          mbar_arrive_expect_tx(fbar, C::kKVTileBytes);
+          for (int r = 0; r < C::kRegions; ++r)
+            tma_load_3d(sring + slot * C::kKVTileBytes + r * C::kKVRegionBytes, map, fbar,
+                        r * 64, tile * kBNX, bh);
+          if (++slot == C::kSlots) {
+            slot = 0;
+            phase ^= 1;
+          }
+        };
+        for (int i = 0; i <= n1; ++i) {
+          if (i < n1) load(&tmap_k, i);
+          if (i >= 1) load(&tmap_v, i - 1);
+        }
+      }
+      __syncwarp();
+    } else if (warp == kXWarpMma) {
+      // ---------------------------------------------------------------- MMA
+      constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBNX, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+      int pos = 0;
+      auto slot_of = [](int r) { return r % C::kSlots; };
+      auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
+      auto wait_full = [&](int r) {
+        mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
+        tc_fence_after();
+      };
+      auto release = [&](int r) { umma_commit_warp(smem_u32(&bars->slot_empty[slot_of(r)])); };
+      const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
+      const uint64_t kdesc = sdesc_sw128(sring, 16, 1024);
+      const uint64_t vdesc = sdesc_sw128(sring, C::kKVRegionBytes, 1024);
+      auto issue_qk = [&](int t, int j, int r) {
+        uint64_t qd = qdesc + uint64_t((t * C::kQTileBytes) >> 4);
+        uint64_t kd = kdesc + uint64_t((slot_of(r) * C::kKVTileBytes) >> 4);
+        asm volatile("" : "+l"(qd), "+l"(kd));
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t qoff = ((ks >> 2) * C::kQRegionBytes + (ks & 3) * 32) >> 4;
+          const uint32_t koff = ((ks >> 2) * C::kKVRegionBytes + (ks & 3) * 32) >> 4;
+          umma_ss_warp(tmem + t * 128 + (j & 1) * kBNX, qd + qoff, kd + koff, idesc_qk, ks > 0);
+        }
+        umma_commit_warp(smem_u32(&bars->s_full[t][j & 1]));
+      };
+      // P of key k of the tile sits in packed column k/2 (k < 32) or 16 + k/2
+      // (each key half over its own first 16 S columns)
+      auto issue_pv = [&](int t, int j, int r) {
+        uint64_t vd = vdesc + uint64_t((slot_of(r) * C::kKVTileBytes) >> 4);
+        asm volatile("" : "+l"(vd));
+        mbar_wait(smem_u32(&bars->p_full[t]), uint32_t(j & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < kBNX / 16; ++ks) {
+          const int pcol = ks * 8 + (ks >= 2 ? 16 : 0);
+          umma_ts_warp(tmem + C::kTmemO + t * D, tmem + t * 128 + (j & 1) * kBNX + pcol,
+                       vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+                       (j > 0 || ks > 0) ? 1u : 0u);
+        }
+        umma_commit_warp(smem_u32(&bars->o_full[t]));
+      };
+      if (n1 > 0) {
+        mbar_wait(smem_u32(&bars->q_full), 0);
+        tc_fence_after();
+        for (int i = 0; i <= n1; ++i) {
+          if (i < n1) {
+            wait_full(pos);
+            if (i < n0) issue_qk(0, i, pos);
+            issue_qk(1, i, pos);
+            release(pos++);
+          }
+          if (i >= 1) {
+            wait_full(pos);
+            if (i - 1 < n0) issue_pv(0, i - 1, pos);
+            issue_pv(1, i - 1, pos);
+            release(pos++);
+          }
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- softmax
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kXRegsSoftmax));
+    const int t = int(warp) >> 3;
+    const int wq = int(warp) & 3;
+    const int rh = (int(warp) >> 2) & 1;
+    const int hl = int(lane) >> 4;                        // key half of the row
+    const int row = wq * 32 + rh * 16 + (int(lane) & 15);  // row in the Q tile
+    const uint32_t lane_off = uint32_t(wq * 32 + rh * 16) << 16;
+    const uint32_t tS0 = tmem + lane_off + t * 128;
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
+    constexpr int kOHalf = D / 2;  // O columns per thread
+    const float sl2 = args.scale_log2;
+    const uint32_t obar = smem_u32(&bars->o_full[t]);
+    const bool tr = kTrace && trace != nullptr && (warp & 7) == 0 && lane == 0;
+    const int key0 = hl * 32;        // first key of my half of the tile
+    const int grow = q0 + t * kBM + row;
+    const int my_n_kv = t == 0 ? n0 : n1;
+
+    float m_run = -INFINITY;  // running max (scaled, log2 units), same in both halves
+    float l_run = 0.f;        // my half's partial normaliser relative to m_run
+
+    for (int j = 0; j < my_n_kv; ++j) {
+      const uint32_t tS = tS0 + (j & 1) * kBNX;
+      mbar_wait(smem_u32(&bars->s_full[t][j & 1]), uint32_t((j >> 1) & 1));
+      tc_fence_after();
+      if (tr) rec(kEvSm0SReady + 5 * t, j);
+      uint32_t sr[32];
+      tmem_ld_16x32bx2_x32<32>(tS, sr);
+      // last admitted key of the tile for this row (MaskSpec::admits,
+      // types.hpp:48-67): ragged tail / padding, causal diagonal
+      int lim = kBNX - 1;
+      if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBNX - 1);
+      if (args.mask == kMaskCausal) lim = min(lim, grow - j * kBNX);
+      const int llim = lim - key0;
+      tmem_wait_ld();
+      reg_fence(sr);
+      float s[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[i] = __uint_as_float(sr[i]);
+      if (__any_sync(0xffffffffu, llim < 31)) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i > llim) s[i] = -INFINITY;
+      }
+      if (tr) rec(kEvSm0Loaded + 5 * t, j);
+      float mx4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mx4[i] = s[i];
+#pragma unroll
+      for (int i = 4; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const float m_new = mx * sl2;
+      if (tr) rec(kEvSm0Max + 5 * t, j);
+      const bool need = m_new > m_run + kRescaleThreshold;
+      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
+      if (need) {
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // O holds PV(0..j-1): wait for PV(j-1), rescale in place (PV(j)
+        // waits for P(j), signalled below)
+        mbar_wait(obar, uint32_t((j - 1) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kOHalf / 16; ++c) {
+          uint32_t orow[16];
+          tmem_ld_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+          tmem_st_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
+        }
+      }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      const uint64_t sl2x2 = f2(sl2, sl2);
+      const uint64_t negm2 = f2(-m_use, -m_use);
+      uint64_t acc[2] = {0ull, 0ull};
+      uint32_t pk[16];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {  // groups of 8 columns
+        uint64_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = ffma2(f2(s[g * 8 + 2 * u], s[g * 8 + 2 * u + 1]), sl2x2, negm2);
+        float p[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#ifdef TA_DEBUG_NO_EXP
+          if (true) {
+            f2_split(x[u], p[2 * u], p[2 * u + 1]);
+          } else
+#endif
+          if (2 * u >= 8 - kEmuPer8) {
+            ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
+          } else {
+            float a, b2;
+            f2_split(x[u], a, b2);
+            p[2 * u] = ex2(a);
+            p[2 * u + 1] = ex2(b2);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[u & 1] = fadd2(acc[u & 1], f2(p[2 * u], p[2 * u + 1]));
+          pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+        }
+      }
+      if (tr) rec(kEvSm0Exp + 5 * t, j);
+      // packed P of my 32 keys -> packed columns [0,16) / [32,48) of the buffer
+      tmem_st_16x32bx2_x16<32>(tS, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t]));
+      {
+        float lo, hi;
+        f2_split(fadd2(acc[0], acc[1]), lo, hi);
+        l_run += lo + hi;
+      }
+      if (tr) rec(kEvSm0PArrive + 5 * t, j);
+    }
+
+    // ------------------------------------------------------------- epilogue
+    // (finalize, tiled.hpp:223-238): O = o / l, RNE to 16 bit; LSE = m + ln l;
+    // rows with no admitted key are zeros with LSE -inf
+    if (my_n_kv > 0) {
+      mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
+      tc_fence_after();
+    }
+    const float l_row = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
+    const float inv_l = l_row > 0.f ? 1.f / l_row : 0.f;
+    uint16_t* orow_g =
+        reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D + hl * kOHalf;
+#pragma unroll
+    for (int c = 0; c < kOHalf / 32; ++c) {
+      uint32_t orow[32];
+      if (my_n_kv > 0) {
+        tmem_ld_16x32bx2_x32<kOHalf>(tO + c * 32, orow);
+        tmem_wait_ld();
+        reg_fence(orow);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) orow[i] = 0u;
+      }
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
+                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
+      if (grow < S) {
+        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                              packed[4 * i + 3]);
+      }
+    }
+    if (args.lse != nullptr && grow < S && hl == 0)
+      args.lse[size_t(bh) * S + grow] =
+          l_row > 0.f ? (m_run + __log2f(l_row)) * kLn2 : -INFINITY;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kXWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
+}
+
+// ----------------------------------------------------------------------------
+// Variant "si" (self-issue): the ping-pong kernel with no MMA warp.  The
+// tensor-core work of a Q tile is issued by its own softmax warpgroup: the
+// last of the 4 warps to finish P part h (smem counter, acq_rel) issues
+// PV part h and, after the last part, S_t(j+1).  This removes the MMA warp's
+// mbarrier wake-up and its in-order coupling of the two tiles from the
+// critical loop S_t(j) -> softmax -> P -> PV_t(j) -> S_t(j+1).
+// ----------------------------------------------------------------------------
+constexpr int kThreadsSI = 384;  // warps 0-7 softmax (2 tiles x 4), 8 TMEM alloc, 9 TMA, 10-11 idle
+
+struct BarriersSI {
+  uint64_t q_full;
+  uint64_t s_full[kQTiles];
+  uint64_t o_full[kQTiles];
+  uint64_t slot_full[8];
+  uint64_t slot_empty[8];  // 2 arrivals: one per Q tile using the slot
+  uint32_t p_cnt[kQTiles][4];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "r"(addr), "r"(v)
+               : "memory");
+  return old;
+}
+
+template <int D, bool kBF16, bool kTrace>
+__global__ void __launch_bounds__(kThreadsSI, 1)
+    sdpa_fwd_si_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                       const __grid_constant__ CUtensorMap tmap_k,
+                       const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sq = smem_u32(smem);
+  const uint32_t sring = sq + kQTiles * C::kTileBytes;
+  BarriersSI* bars = reinterpret_cast<BarriersSI*>(smem + C::kSmemData);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int S = args.seq_len;
+  const int bh = blockIdx.y;
+  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
+  const int q0 = qblk * (kBM * kQTiles);
+  const int kv_len =
+      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
+  const int n_kv_seq = (kv_len + kBN - 1) / kBN;
+  const int diag0 = q0 / kBN;
+  const int n0 = args.mask == kMaskCausal ? min(diag0 + 1, n_kv_seq) : n_kv_seq;
+  const int n1 = args.mask == kMaskCausal ? min(diag0 + 2, n_kv_seq) : n_kv_seq;
+  long long* const trace = (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+  auto rec = [&](int ev, int j) {
+    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
+  };
+
+  if (threadIdx.x == kWarpTma * 32) {
+    mbar_init(smem_u32(&bars->q_full), 1);
+    for (int t = 0; t < kQTiles; ++t) {
+      mbar_init(smem_u32(&bars->s_full[t]), 1);
+      mbar_init(smem_u32(&bars->o_full[t]), 1);
+      for (int h = 0; h < 4; ++h) bars->p_cnt[t][h] = 0;
+    }
+    for (int s = 0; s < C::kSlots; ++s) {
+      mbar_init(smem_u32(&bars->slot_full[s]), 1);
+      mbar_init(smem_u32(&bars->slot_empty[s]), 2);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp >= kNumSoftmaxWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
+    if (warp == kWarpTma && lane == 0 && n1 > 0) {
+      // ---------------------------------------------------------------- TMA
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+      const uint32_t qbar = smem_u32(&bars->q_full);
+      mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
+      for (int t = 0; t < kQTiles; ++t)
+        for (int r = 0; r < C::kRegions; ++r)
+          tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
+                      q0 + t * kBM, bh);
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n1; ++j) {
+        for (int kv = 0; kv < 2; ++kv) {
+          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
+          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+          mbar_arrive_expect_tx(fbar, C::kTileBytes);
+          const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
+          for (int r = 0; r < C::kRegions; ++r)
+            tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
+                        j * kBN, bh);
+          if (++slot == C::kSlots) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- softmax
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    const int t = warp / 4;
+    const uint32_t wq = warp & 3;
+    const int row = int(wq * 32 + lane);
+    const uint32_t lane_off = (wq * 32u) << 16;
+    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN;
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
+    const float sl2 = args.scale_log2;
+    const uint32_t sbar = smem_u32(&bars->s_full[t]);
+    const uint32_t obar = smem_u32(&bars->o_full[t]);
+    const bool tr = kTrace && trace != nullptr && row == 0;
+    const int my_n = t == 0 ? n0 : n1;
+
+    // ---- tensor-core issue (one elected lane of the issuing warp)
+    constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
+    constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+    // ring position r: K_j at 2j, V_j at 2j+1
+    auto slot_of = [](int r) { return r % C::kSlots; };
+    auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
+    // K_j / V_j are used by Q tile 0 only while j < n0: tile 1 releases for both after that
+    auto release = [&](int r) {
+      const uint32_t b = smem_u32(&bars->slot_empty[slot_of(r)]);
+      umma_commit_warp(b);
+      if (t == 1 && (r >> 1) >= n0) umma_commit_warp(b);
+    };
+    auto issue_qk = [&](int j) {
+      const int r = 2 * j;
+      mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
+      tc_fence_after();
+      uint64_t qd = sdesc_sw128(sq + t * C::kTileBytes, 16, 1024);
+      uint64_t kd = sdesc_sw128(sring + slot_of(r) * C::kTileBytes, 16, 1024);
+      asm volatile("" : "+l"(qd), "+l"(kd));
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
+        umma_ss_warp(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
+      }
+      umma_commit_warp(sbar);
+      release(r);
+    };
+    auto issue_pv_part = [&](int j, int h) {
+      const int r = 2 * j + 1;
+      if (h == 0) {
+        mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
+        tc_fence_after();
+      }
+      uint64_t vd = sdesc_sw128(sring + slot_of(r) * C::kTileBytes, C::kRegionBytes, 1024);
+      asm volatile("" : "+l"(vd));
+#pragma unroll
+      for (int kk = 0; kk < kBN / 16 / kPParts; ++kk) {
+        const int ks = h * (kBN / 16 / kPParts) + kk;
+        umma_ts_warp(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
+                     vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv, (j > 0 || ks > 0) ? 1u : 0u);
+      }
+      if (h == kPParts - 1) {
+        umma_commit_warp(obar);
+        release(r);
+      }
+    };
+
+    if (wq == 0 && my_n > 0) {  // S_t(0)
+      mbar_wait(smem_u32(&bars->q_full), 0);
+      tc_fence_after();
+      issue_qk(0);
+    }
+
+    float m_run = -INFINITY;  // running max used for the exponent (scaled, log2 units)
+    float l_run = 0.f;        // running normaliser relative to m_run
+
+    for (int j = 0; j < my_n; ++j) {
+      mbar_wait(sbar, uint32_t(j & 1));
+      tc_fence_after();
+      if (tr) rec(kEvSm0SReady + 5 * t, j);
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
+      int lim = kBN - 1;
+      if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
+      if (args.mask == kMaskCausal && j == diag0 + t) lim = min(lim, row);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
+      if (lim < kBN - 1) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i > lim) s[i] = -INFINITY;
+      }
+      if (tr) rec(kEvSm0Loaded + 5 * t, j);
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+#pragma unroll
+      for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float m_new = mx * sl2;
+      if (tr) rec(kEvSm0Max + 5 * t, j);
+      const bool need = m_new > m_run + kRescaleThreshold;
+      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
+      if (need) {
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // O holds PV(0..j-1): wait for PV(j-1), rescale in place (PV(j) is
+        // issued only after all 4 warps have written P part 0 below)
+        mbar_wait(obar, uint32_t((j - 1) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orow[32];
+          tmem_ld32(tO + c * 32, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+          tmem_st32(tO + c * 32, orow);
+        }
+      }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      const uint64_t sl2x2 = f2(sl2, sl2);
+      const uint64_t negm2 = f2(-m_use, -m_use);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+      for (int h = 0; h < kPParts; ++h) {
+        constexpr int kCols = kBN / kPParts;
+        uint32_t pk[kCols / 32][16];
+#pragma unroll
+        for (int g = 0; g < kCols / 8; ++g) {
+          const int c0 = h * kCols + g * 8;
+          uint64_t x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
+          float p[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#ifdef TA_DEBUG_NO_EXP
+            if (true) {
+              f2_split(x[u], p[2 * u], p[2 * u + 1]);
+            } else
+#endif
+            if (2 * u >= 8 - kEmuPer8) {
+              ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
+            } else {
+              float a, b;
+              f2_split(x[u], a, b);
+              p[2 * u] = ex2(a);
+              p[2 * u + 1] = ex2(b);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
+            pk[(g * 4 + u) / 16][(g * 4 + u) % 16] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < kCols / 32; ++i) tmem_st16(tS + h * (kCols / 2) + i * 16, pk[i]);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        // the last of the tile's 4 warps to land P part h issues PV part h
+        uint32_t last = 0;
+        if (lane == 0) {
+          const uint32_t cnt = smem_u32(&bars->p_cnt[t][h]);
+          last = atom_add_acq_rel(cnt, 1u) == 3u;
+          if (last) st_shared_relaxed(cnt, 0u);
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          tc_fence_after();
+          issue_pv_part(j, h);
+          if (h == kPParts - 1 && j + 1 < my_n) issue_qk(j + 1);
+          if (h == kPParts - 1 && tr) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
+        }
+        if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
+      }
+      {
+        const uint64_t a01 = fadd2(acc[0], acc[1]);
+        const uint64_t a23 = fadd2(acc[2], acc[3]);
+        float lo, hi;
+        f2_split(fadd2(a01, a23), lo, hi);
+        l_run += lo + hi;
+      }
+      if (tr) rec(kEvSm0PArrive + 5 * t, j);
+    }
+
+    // ------------------------------------------------------------- epilogue
+    if (my_n > 0) {
+      mbar_wait(obar, uint32_t((my_n - 1) & 1));
+      tc_fence_after();
+    }
+    const int grow = q0 + t * kBM + row;
+    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t orow[32];
+      if (my_n > 0) {
+        tmem_ld32(tO + c * 32, orow);
+        tmem_wait_ld();
+        reg_fence(orow);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) orow[i] = 0u;
+      }
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
+                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
+      if (grow < S) {
+        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                              packed[4 * i + 3]);
+      }
+    }
+    if (args.lse != nullptr && grow < S)
+      args.lse[size_t(bh) * S + grow] =
+          l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
+}
+
+template <int D, bool kBF16>
+cudaError_t launch_si(const FwdLaunch& L) {
+  using C = Cfg<D>;
+  auto kern = L.args.trace != nullptr ? sdpa_fwd_si_kernel<D, kBF16, true>
+                                      : sdpa_fwd_si_kernel<D, kBF16, false>;
+  static bool attr_set[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int tr = L.args.trace != nullptr;
+  if (dev < 64 && !attr_set[dev][tr]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set[dev][tr] = true;
+  }
+  const int rows_per_cta = kBM * kQTiles;
+  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
+  kern<<<grid, kThreadsSI, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------------
@@ -930,8 +2031,55 @@ cudaError_t launch_db(const FwdLaunch& L) {
 }
 
 template <int D, bool kBF16>
+cudaError_t launch_rs(const FwdLaunch& L) {
+  using C = Cfg<D>;
+  auto kern = L.args.trace != nullptr ? sdpa_fwd_rs_kernel<D, kBF16, true>
+                                      : sdpa_fwd_rs_kernel<D, kBF16, false>;
+  static bool attr_set[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int tr = L.args.trace != nullptr;
+  if (dev < 64 && !attr_set[dev][tr]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set[dev][tr] = true;
+  }
+  const int rows_per_cta = kBM * kQTiles;
+  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
+  kern<<<grid, kThreadsRS, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
+  return cudaGetLastError();
+}
+
+template <int D, bool kBF16>
+cudaError_t launch_x(const FwdLaunch& L) {
+  using C = CfgX<D>;
+  auto kern = L.args.trace != nullptr ? sdpa_fwd_x_kernel<D, kBF16, true>
+                                      : sdpa_fwd_x_kernel<D, kBF16, false>;
+  static bool attr_set[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int tr = L.args.trace != nullptr;
+  if (dev < 64 && !attr_set[dev][tr]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set[dev][tr] = true;
+  }
+  const int rows_per_cta = kBM * kQTiles;
+  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
+  kern<<<grid, kThreadsX, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
+  return cudaGetLastError();
+}
+
+template <int D, bool kBF16>
 cudaError_t launch_typed(const FwdLaunch& L) {
+  if (L.variant == 4) return launch_si<D, kBF16>(L);
+  if (L.variant == 3) return launch_x<D, kBF16>(L);
   if (L.variant == 1) return launch_db<D, kBF16>(L);
+  if (L.variant == 2) return launch_rs<D, kBF16>(L);
   using C = Cfg<D>;
   auto kern = sdpa_fwd_kernel<D, kBF16>;
   static bool attr_set[64] = {};  // per device
@@ -955,14 +2103,15 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 FwdGeometry fwd_geometry(int64_t S, int64_t BH, int variant) {
   FwdGeometry g;
   g.block_m = kBM;
-  g.block_n = kBN;
+  g.block_n = variant == 3 ? kBNX : kBN;
   g.q_tiles_per_cta = variant == 1 ? 1 : kQTiles;
-  g.threads = variant == 1 ? kThreadsDB : kThreads;
+  g.threads = variant == 1 ? kThreadsDB : variant == 2 ? kThreadsRS : variant == 3 ? kThreadsX : kThreads;
   g.ctas = ((S + kBM * g.q_tiles_per_cta - 1) / (kBM * g.q_tiles_per_cta)) * BH;
   return g;
 }
 
 int fwd_ring_slots(int D, int variant) {
+  if (variant == 3) return D == 128 ? CfgX<128>::kSlots : CfgX<64>::kSlots;
   if (variant == 1) return D == 128 ? CfgDB<128>::kSlots : CfgDB<64>::kSlots;
   return D == 128 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
 }

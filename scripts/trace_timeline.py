@@ -30,9 +30,10 @@ print("mean over iters 8..n-2 (cycles):")
 print(" period s0Ready->s0Ready", np.mean([t[4, j + 1] - t[4, j] for j in js]))
 print(" s0: ready->load %.0f load->max %.0f max->exp %.0f exp->arrive %.0f" % (d(4, 5), d(5, 6), d(6, 7), d(7, 8)))
 print(" s1: ready->load %.0f load->max %.0f max->exp %.0f exp->arrive %.0f" % (d(9, 10), d(10, 11), d(11, 12), d(12, 13)))
-print(" s0 arrive(j) -> mma sees P0(j) [next iter]:", np.mean([t[0, j + 1] - t[8, j] for j in js]))
-print(" mma issued PV0,S0(j+1) -> s0 ready(j+1):", np.mean([t[4, j + 1] - t[1, j + 1] for j in js]))
-print(" s1 arrive(j) -> mma sees P1(j):", np.mean([t[2, j + 1] - t[13, j] for j in js]))
+print(" s0 arrive(j) -> mma sees P0(j):", np.mean([t[0, j] - t[8, j] for j in js]))
+print(" mma saw P0(j) -> PV0(j) issued:", np.mean([t[1, j] - t[0, j] for j in js]))
+print(" s1 arrive(j) -> mma sees P1(j):", np.mean([t[2, j] - t[13, j] for j in js]))
+print(" PV0(j) issued -> s0 ready(j+1):", np.mean([t[4, j + 1] - t[1, j] for j in js]))
 print(" TC: PV0(j) done -> S0(j+1) done %.0f" % d(14, 15))
 print(" TC: S0(j+1) done -> PV1(j) done %.0f" % d(15, 16))
 print(" TC: PV1(j) done -> S1(j+1) done %.0f" % d(16, 17))
