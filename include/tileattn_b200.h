@@ -151,7 +151,7 @@ TA_API ta_status ta_debug_umma_gemm(int mode, ta_dtype dtype, const void* a, con
                              void* stream);
 
 /* Diagnostics: run the forward once with a cycle-timeline trace of CTA (0,0):
- * trace (device, int64[18 * 64]) receives clock64 stamps per event and K/V
+ * trace (device, int64[24 * 64]) receives clock64 stamps per event and K/V
  * iteration (event ids: see TraceEvent in csrc/sdpa_fwd_sm100.h).  Synchronous. */
 TA_API ta_status ta_debug_sdpa_trace(const void* q, const void* k, const void* v, void* o,
                                      ta_shape shape, ta_dtype dtype, long long* trace,

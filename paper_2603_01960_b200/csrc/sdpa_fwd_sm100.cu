@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <type_traits>
 
 #include "ptx_sm100.cuh"
 #include "sdpa_fwd_sm100.h"
@@ -36,10 +37,20 @@ constexpr int kThreads = 384;   // 12 warps
 // Warp roles.  The SM's warp arbiter favours the highest warp id among
 // eligible warps, so the latency-critical single-thread roles (MMA issue, TMA)
 // take the top ids and are never starved by the softmax warps' issue stream.
-constexpr int kNumSoftmaxWarps = 8;  // warps 0..3 -> Q tile 0, 4..7 -> Q tile 1
-constexpr int kWarpAlloc = 8;        // TMEM allocator (otherwise idle)
-constexpr int kWarpTma = 9;
-constexpr int kWarpMma = 11;
+constexpr int kNumSoftmaxWarps = 8;  // softmax warps s = 0..3 -> Q tile 0, 4..7 -> Q tile 1
+// Control warps either below (TA_CONTROL_LOW) or above the softmax warps.
+// The warp scheduler prefers higher warp ids: control-high gives the MMA
+// warp priority on its SMSP (fast issue), control-low gives the softmax
+// warp sharing that SMSP priority (less skew between the 4 softmax warps).
+#ifndef TA_CONTROL_LOW
+#define TA_CONTROL_LOW 0
+#endif
+constexpr int kSoftmaxBase = TA_CONTROL_LOW ? 4 : 0;  // first softmax warp
+constexpr int kCtl = TA_CONTROL_LOW ? 0 : 8;          // first control warp
+constexpr int kWarpAlloc = kCtl + 0;  // TMEM allocator (otherwise idle)
+constexpr int kWarpTma = kCtl + 1;
+constexpr int kWarpTrace = kCtl + 2;  // diagnostics only
+constexpr int kWarpMma = kCtl + 3;
 constexpr uint32_t kTmemCols = 512;
 // register split: 4 control warps (TMA, MMA, TMEM alloc, spare) + 8 softmax warps
 // setmaxnreg.inc only draws on registers released by setmaxnreg.dec in the
@@ -58,14 +69,30 @@ constexpr float kRescaleThreshold = 8.0f;
 // exp2 work split: of every 8 score columns, kEmuPer8 use the FMA-pipe
 // polynomial (ex2_poly) and the rest the MUFU (measured 16 exp2/clk/SM).
 #ifndef TA_EMU_PER8
-#define TA_EMU_PER8 2
+#define TA_EMU_PER8 1
 #endif
 constexpr int kEmuPer8 = TA_EMU_PER8;
+#ifndef TA_EMU_Q3
+#define TA_EMU_Q3 TA_EMU_PER8
+#endif
+constexpr int kEmuQ3 = TA_EMU_Q3;
 // P hand-off granularity to the PV MMAs (2 = halves, 4 = quarters of 32 keys)
 #ifndef TA_P_PARTS
 #define TA_P_PARTS 2
 #endif
 constexpr int kPParts = TA_P_PARTS;
+// Stale max: after the first K/V tile, exponentiate against the running max
+// without a per-tile row max; a P part whose row sum exceeds 2^8 (some p may
+// exceed the lazy-rescale bound) takes the slow path.
+#ifndef TA_STALE_MAX
+#define TA_STALE_MAX 1
+#endif
+constexpr bool kStaleMax = TA_STALE_MAX != 0;
+constexpr float kSumGuard = 256.0f;
+// MMA issue: 4 K-steps per elect (1) or one elect per K-step (0)
+#ifndef TA_MMA_BATCH
+#define TA_MMA_BATCH 1
+#endif
 
 template <int D>
 struct Cfg {
@@ -84,17 +111,22 @@ struct Barriers {
   uint64_t s_full[kQTiles];
   uint64_t p_full[kQTiles][4];  // P key columns [32q, 32q+32) written (q < kPParts)
   uint64_t o_full[kQTiles];
+  uint64_t o_half[kQTiles];  // PV(j) over P part 0 complete (stale-max slow path)
   uint64_t slot_full[8];
   uint64_t slot_empty[8];
   uint32_t tmem_base;
 };
 
-template <int D, bool kBF16>
+template <int D, bool kBF16, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
   using C = Cfg<D>;
+  // the stale-max softmax pays off where the softmax is on the critical path
+  // of a tensor-bound loop (D=128); at D=64 the kernel is softmax-throughput
+  // bound and the extra o_half commit costs more than the saved row max
+  constexpr bool kStale = kStaleMax && D == 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -122,8 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int t = 0; t < kQTiles; ++t)
     n_kv_t[t] = args.mask == kMaskCausal ? min(diag0 + t + 1, n_kv_seq) : n_kv_seq;
   const int n_kv = n_kv_t[kQTiles - 1];  // K/V tiles streamed (max over the Q tiles)
-  long long* const trace =
-      (args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+  long long* const trace = (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
   auto rec = [&](int ev, int j) {
     if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
   };
@@ -135,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int q = 0; q < kPParts; ++q)
         mbar_init(smem_u32(&bars->p_full[t][q]), kBM / 32);  // one arrive per warp
       mbar_init(smem_u32(&bars->o_full[t]), 1);
+      mbar_init(smem_u32(&bars->o_half[t]), 1);
     }
     for (int s = 0; s < C::kSlots; ++s) {
       mbar_init(smem_u32(&bars->slot_full[s]), 1);
@@ -148,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp >= kNumSoftmaxWarps) {
+  if (warp - kSoftmaxBase >= uint32_t(kNumSoftmaxWarps)) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
   if (warp == kWarpTma) {
     // ------------------------------------------------------------------ TMA
@@ -180,9 +212,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kWarpMma - 1) {
+  } else if (warp == kWarpTrace) {
     // optional tracer: timestamps of tensor-core completions (diagnostics only)
-    if (lane == 0 && trace != nullptr) {
+    if (kTrace && lane == 0 && trace != nullptr) {
       for (int j = 0; j < n_kv && j < kTraceIters; ++j) {
         mbar_wait(smem_u32(&bars->o_full[0]), uint32_t(j & 1));
         rec(kEvTcPV0Done, j);
@@ -221,33 +253,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_qk = [&](int t, int r) {
         uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
         uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-        // opaque to the optimiser: stops 2 x 8 per-K-step descriptors being
-        // hoisted out of the K/V loop into (spilled) registers
+#if TA_MMA_BATCH
+#pragma unroll
+        for (int r = 0; r < C::kRegions; ++r) {  // 4 K-steps of 16 per 128-B swizzle region
+          const uint32_t off = (r * C::kRegionBytes) >> 4;
+          umma_ss_x4<2, 2>(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, r > 0);
+        }
+#else
         asm volatile("" : "+l"(qd), "+l"(kd));
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
           umma_ss_warp(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
         }
+#endif
         umma_commit_warp(smem_u32(&bars->s_full[t]));
       };
       // PV in two halves of 64 keys, each issued as soon as the softmax
       // warpgroup has written that half of P (P aliases S in TMEM).
       auto issue_pv = [&](int t, int r, bool accumulate, int j) {
         uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-        asm volatile("" : "+l"(vd));
 #pragma unroll
         for (int h = 0; h < kPParts; ++h) {
           mbar_wait(smem_u32(&bars->p_full[t][h]), uint32_t(j & 1));
           tc_fence_after();
           if (h == kPParts - 1 && lane == 0) rec(t == 0 ? kEvMmaWaitP0 : kEvMmaWaitP1, j);
+          static_assert(kBN / 16 / kPParts == 4, "P part = 4 K-steps of 16 keys");
+          const int ks0 = h * 4;
+#if TA_MMA_BATCH
+          constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
+          umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks0 * 8,
+                             vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv,
+                             (accumulate || h > 0) ? 1u : 0u);
+#else
+          asm volatile("" : "+l"(vd));
 #pragma unroll
-          for (int kk = 0; kk < kBN / 16 / kPParts; ++kk) {
-            const int ks = h * (kBN / 16 / kPParts) + kk;
+          for (int kk = 0; kk < 4; ++kk) {
+            const int ks = ks0 + kk;
             umma_ts_warp(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
-                    vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
-                    (accumulate || ks > 0) ? 1u : 0u);
+                         vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+                         (accumulate || ks > 0) ? 1u : 0u);
           }
+#endif
+          if (kStale && h == 0) umma_commit_warp(smem_u32(&bars->o_half[t]));
         }
         umma_commit_warp(smem_u32(&bars->o_full[t]));
         if (lane == 0) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
@@ -284,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // -------------------------------------------------------------- softmax
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-    const int t = warp / 4;
+    const int t = int(warp - kSoftmaxBase) / 4;
     const uint32_t wq = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = int(wq * 32 + lane);
     const uint32_t lane_off = (wq * 32u) << 16;
@@ -301,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < my_n_kv; ++j) {
       mbar_wait(sbar, uint32_t(j & 1));
       tc_fence_after();
-      const bool tr = (row == 0);
+      const bool tr = kTrace && row == 0;
       if (tr) rec(kEvSm0SReady + 5 * t, j);
       uint32_t sr[4][32];
 #pragma unroll
@@ -330,7 +378,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (i > lim) s[i] = -INFINITY;
         }
       }
-      // row max (8 independent chains)
+      // row max (8 independent chains); with kStale only on the first
+      // tile: later tiles exponentiate against the running max directly and
+      // the half-row sum guards the lazy-rescale invariant (below)
+      if (!kStale || j == 0) {
       float mx8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = s[i];
@@ -364,17 +415,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(tO + c * 32, orow);
         }
       }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      }
+      float m_use = m_run == -INFINITY ? 0.f : m_run;
       // x = s * scale*log2e - m as packed FFMA2; exp2 split between the MUFU
       // and the FMA pipe (kEmuPer8 of every 8 columns, emulated in pairs);
       // row sum as packed FADD2 into 4 pair accumulators.
       const uint64_t sl2x2 = f2(sl2, sl2);
-      const uint64_t negm2 = f2(-m_use, -m_use);
-      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+      // exps of the row in kPParts parts; E of every 8 columns on the FMA pipe
+      auto exps = [&](auto emu) {
+      constexpr int E = decltype(emu)::value;
 #pragma unroll
       for (int h = 0; h < kPParts; ++h) {
         constexpr int kCols = kBN / kPParts;  // key columns per P part
         uint32_t pk[kCols / 32][16];
+        uint64_t acc[4];
+        auto part_exps = [&]() {
+        const uint64_t negm2 = f2(-m_use, -m_use);
+        acc[0] = acc[1] = acc[2] = acc[3] = 0ull;
 #pragma unroll
         for (int g = 0; g < kCols / 8; ++g) {  // groups of 8 columns
           const int c0 = h * kCols + g * 8;
@@ -391,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               f2_split(x[u], p[2 * u], p[2 * u + 1]);
             } else
 #endif
-            if (2 * u >= 8 - kEmuPer8) {
+            if (2 * u >= 8 - E) {
               ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
             } else {
               float a, b;
@@ -406,6 +463,58 @@ __global__ void __launch_bounds__(kThreads, 1)
             pk[(g * 4 + u) / 16][(g * 4 + u) % 16] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
           }
         }
+        };
+        part_exps();
+        float psum;
+        {
+          const uint64_t a01 = fadd2(acc[0], acc[1]);
+          const uint64_t a23 = fadd2(acc[2], acc[3]);
+          float lo, hi;
+          f2_split(fadd2(a01, a23), lo, hi);
+          psum = lo + hi;
+        }
+        if (kStale && j > 0 && __any_sync(0xffffffffu, !(psum <= kSumGuard))) {
+          // rare: some p of this part may exceed 2^8 (or overflowed): move
+          // m_run to the part's max, rescale l and O, redo the part.  O is
+          // stable here: PV(j-1) (part 0) or PV(j) over the earlier parts
+          // (o_half) has landed; this part is not yet handed off.
+          float hm4[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) hm4[i] = s[h * kCols + i];
+#pragma unroll
+          for (int i = 4; i < kCols; ++i) hm4[i & 3] = fmaxf(hm4[i & 3], s[h * kCols + i]);
+          const float m_part = fmaxf(fmaxf(hm4[0], hm4[1]), fmaxf(hm4[2], hm4[3])) * sl2;
+          const bool need = !(psum <= kSumGuard) && m_part > m_run;
+          const float alpha = need ? ex2(m_run - m_part) : 1.f;
+          if (need) {
+            l_run *= alpha;
+            m_run = m_part;
+            m_use = m_run;
+          }
+          if (h == 0)
+            mbar_wait(obar, uint32_t((j - 1) & 1));
+          else
+            mbar_wait(smem_u32(&bars->o_half[t]), uint32_t(j & 1));
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D / 16; ++c) {
+            uint32_t orow[16];
+            tmem_ld16(tO + c * 16, orow);
+            tmem_wait_ld();
+            reg_fence(orow);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+            tmem_st16(tO + c * 16, orow);
+          }
+          part_exps();
+          const uint64_t a01 = fadd2(acc[0], acc[1]);
+          const uint64_t a23 = fadd2(acc[2], acc[3]);
+          float lo, hi;
+          f2_split(fadd2(a01, a23), lo, hi);
+          psum = lo + hi;
+        }
+        l_run += psum;
 #pragma unroll
         for (int i = 0; i < kCols / 32; ++i) tmem_st16(tS + h * (kCols / 2) + i * 16, pk[i]);
         tmem_wait_st();
@@ -413,14 +522,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
         if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
+        if (kTrace && h == kPParts - 1 && t == 0 && wq > 0 && lane == 0)
+          rec(kEvSm0ArriveW1 + int(wq) - 1, j);
       }
-      {
-        const uint64_t a01 = fadd2(acc[0], acc[1]);
-        const uint64_t a23 = fadd2(acc[2], acc[3]);
-        float lo, hi;
-        f2_split(fadd2(a01, a23), lo, hi);
-        l_run += lo + hi;
-      }
+      };
+      // the MMA warp shares SMSP 3 (lane quadrant 3): its softmax warps trade
+      // FMA-pipe emulation (issue slots) for MUFU time
+      if (kEmuQ3 != kEmuPer8 && wq == 3)
+        exps(std::integral_constant<int, kEmuQ3>{});
+      else
+        exps(std::integral_constant<int, kEmuPer8>{});
       if (tr) rec(kEvSm0PArrive + 5 * t, j);
     }
 
@@ -839,1091 +950,6 @@ __global__ void __launch_bounds__(kThreadsRS, 1)
 }
 
 // ----------------------------------------------------------------------------
-// Variant "x" (default): 64-key K/V tiles with double-buffered S per Q tile.
-// TMEM: S(t, b) at columns 128 t + 64 b (fp32, P written over it in 16-bit),
-// O(t) at 256 + D t.  The tensor core computes S(j+1) of both Q tiles while
-// the softmax of S(j) runs, so the softmax's TMEM-read latency and its exps
-// are no longer in series with the MMA round trip: the loop runs at
-// max(tensor time, softmax throughput) instead of their sum.  16 softmax
-// warps as in "rs" (two threads per row, 32 keys each per tile).
-// MMA issue order: S0(0) S1(0) | S0(1) S1(1) PV0(0) PV1(0) | S0(2) S1(2) PV0(1)..
-// (S_t(j+2) reuses the buffer PV_t(j) has read: in-order tensor pipe).
-// ----------------------------------------------------------------------------
-constexpr int kBNX = 64;         // keys per K/V tile
-constexpr int kThreadsX = 640;   // 20 warps: 16 softmax + TMEM alloc, TMA, spare, MMA
-constexpr int kXWarpAlloc = 16, kXWarpTma = 17, kXWarpMma = 19;
-constexpr int kXRegsControl = 56;
-constexpr int kXRegsSoftmax = 104;
-static_assert(16 * 32 * (kXRegsSoftmax - kRSLaunchRegs) <= 4 * 32 * (kRSLaunchRegs - kXRegsControl),
-              "setmaxnreg.inc would wait forever: register pool does not balance");
-
-template <int D>
-struct CfgX {
-  static constexpr int kRegions = D / 64;
-  static constexpr int kQTileBytes = kBM * D * 2;
-  static constexpr int kQRegionBytes = kBM * 128;
-  static constexpr int kKVTileBytes = kBNX * D * 2;
-  static constexpr int kKVRegionBytes = kBNX * 128;
-  static constexpr int kSlots = D == 128 ? 8 : 16;
-  static constexpr int kSmemData = kQTiles * kQTileBytes + kSlots * kKVTileBytes;
-  static constexpr int kSmemBytes = kSmemData + 1024 + 1024;
-  static constexpr uint32_t kTmemO = 256;
-};
-
-struct BarriersX {
-  uint64_t q_full;
-  uint64_t s_full[kQTiles][2];  // [tile][S buffer]
-  uint64_t p_full[kQTiles];     // P_t(j) written (8 warp arrivals)
-  uint64_t o_full[kQTiles];     // PV_t(j) complete
-  uint64_t slot_full[16];
-  uint64_t slot_empty[16];
-  uint32_t tmem_base;
-};
-
-template <int D, bool kBF16, bool kTrace>
-__global__ void __launch_bounds__(kThreadsX, 1)
-    sdpa_fwd_x_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                      const __grid_constant__ CUtensorMap tmap_k,
-                      const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
-  using C = CfgX<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  const uint32_t sq = smem_u32(smem);
-  const uint32_t sring = sq + kQTiles * C::kQTileBytes;
-  BarriersX* bars = reinterpret_cast<BarriersX*>(smem + C::kSmemData);
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();
-  const int S = args.seq_len;
-  const int bh = blockIdx.y;
-  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
-  const int q0 = qblk * (kBM * kQTiles);
-  const int kv_len =
-      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
-  const int n_kv_seq = (kv_len + kBNX - 1) / kBNX;
-  // trip counts (causal: kv_end = last_row / t_n + 1, tiled.cpp:159)
-  const int n0 = args.mask == kMaskCausal ? min((q0 + kBM - 1) / kBNX + 1, n_kv_seq) : n_kv_seq;
-  const int n1 =
-      args.mask == kMaskCausal ? min((q0 + 2 * kBM - 1) / kBNX + 1, n_kv_seq) : n_kv_seq;
-  long long* const trace = (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
-  auto rec = [&](int ev, int j) {
-    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
-  };
-
-  if (threadIdx.x == kXWarpMma * 32) {
-    mbar_init(smem_u32(&bars->q_full), 1);
-    for (int t = 0; t < kQTiles; ++t) {
-      mbar_init(smem_u32(&bars->s_full[t][0]), 1);
-      mbar_init(smem_u32(&bars->s_full[t][1]), 1);
-      mbar_init(smem_u32(&bars->p_full[t]), 8);
-      mbar_init(smem_u32(&bars->o_full[t]), 1);
-    }
-    for (int s = 0; s < C::kSlots; ++s) {
-      mbar_init(smem_u32(&bars->slot_full[s]), 1);
-      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == kXWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp >= 16) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kXRegsControl));
-    if (warp == kXWarpTma) {
-      // ---------------------------------------------------------------- TMA
-      // ring order = MMA consumption order: K0 | K1 V0 | K2 V1 | ... | V(n-1)
-      if (lane == 0 && n1 > 0) {
-        tma_prefetch_desc(&tmap_q);
-        tma_prefetch_desc(&tmap_k);
-        tma_prefetch_desc(&tmap_v);
-        const uint32_t qbar = smem_u32(&bars->q_full);
-        mbar_arrive_expect_tx(qbar, kQTiles * C::kQTileBytes);
-        for (int t = 0; t < kQTiles; ++t)
-          for (int r = 0; r < C::kRegions; ++r)
-            tma_load_3d(sq + t * C::kQTileBytes + r * C::kQRegionBytes, &tmap_q, qbar, r * 64,
-                        q0 + t * kBM, bh);
-        int slot = 0;
-        uint32_t phase = 0;
-        auto load = [&](const CUtensorMap* map, int tile) {
-          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
-          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-          mbar_arrive_expect_tx(fbar, C::kKVTileBytes);
-          for (int r = 0; r < C::kRegions; ++r)
-            tma_load_3d(sring + slot * C::kKVTileBytes + r * C::kKVRegionBytes, map, fbar,
-                        r * 64, tile * kBNX, bh);
-          if (++slot == C::kSlots) {
-            slot = 0;
-            phase ^= 1;
-          }
-        };
-        for (int i = 0; i <= n1; ++i) {
-          if (i < n1) load(&tmap_k, i);
-          if (i >= 1) load(&tmap_v, i - 1);
-        }
-      }
-      __syncwarp();
-    } else if (warp == kXWarpMma) {
-      // ---------------------------------------------------------------- MMA
-      constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBNX, false, false);
-      constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
-      int pos = 0;
-      auto slot_of = [](int r) { return r % C::kSlots; };
-      auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
-      auto wait_full = [&](int r) {
-        mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
-        tc_fence_after();
-      };
-      auto release = [&](int r) { umma_commit_warp(smem_u32(&bars->slot_empty[slot_of(r)])); };
-      const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
-      const uint64_t kdesc = sdesc_sw128(sring, 16, 1024);
-      const uint64_t vdesc = sdesc_sw128(sring, C::kKVRegionBytes, 1024);
-      auto issue_qk = [&](int t, int j, int r) {
-        uint64_t qd = qdesc + uint64_t((t * C::kQTileBytes) >> 4);
-        uint64_t kd = kdesc + uint64_t((slot_of(r) * C::kKVTileBytes) >> 4);
-        asm volatile("" : "+l"(qd), "+l"(kd));
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t qoff = ((ks >> 2) * C::kQRegionBytes + (ks & 3) * 32) >> 4;
-          const uint32_t koff = ((ks >> 2) * C::kKVRegionBytes + (ks & 3) * 32) >> 4;
-          umma_ss_warp(tmem + t * 128 + (j & 1) * kBNX, qd + qoff, kd + koff, idesc_qk, ks > 0);
-        }
-        umma_commit_warp(smem_u32(&bars->s_full[t][j & 1]));
-      };
-      // P of key k of the tile sits in packed column k/2 (k < 32) or 16 + k/2
-      // (each key half over its own first 16 S columns)
-      auto issue_pv = [&](int t, int j, int r) {
-        uint64_t vd = vdesc + uint64_t((slot_of(r) * C::kKVTileBytes) >> 4);
-        asm volatile("" : "+l"(vd));
-        mbar_wait(smem_u32(&bars->p_full[t]), uint32_t(j & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < kBNX / 16; ++ks) {
-          const int pcol = ks * 8 + (ks >= 2 ? 16 : 0);
-          umma_ts_warp(tmem + C::kTmemO + t * D, tmem + t * 128 + (j & 1) * kBNX + pcol,
-                       vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
-                       (j > 0 || ks > 0) ? 1u : 0u);
-        }
-        umma_commit_warp(smem_u32(&bars->o_full[t]));
-      };
-      if (n1 > 0) {
-        mbar_wait(smem_u32(&bars->q_full), 0);
-        tc_fence_after();
-        for (int i = 0; i <= n1; ++i) {
-          if (i < n1) {
-            wait_full(pos);
-            if (i < n0) issue_qk(0, i, pos);
-            issue_qk(1, i, pos);
-            release(pos++);
-          }
-          if (i >= 1) {
-            wait_full(pos);
-            if (i - 1 < n0) issue_pv(0, i - 1, pos);
-            issue_pv(1, i - 1, pos);
-            release(pos++);
-          }
-        }
-      }
-    }
-  } else {
-    // -------------------------------------------------------------- softmax
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kXRegsSoftmax));
-    const int t = int(warp) >> 3;
-    const int wq = int(warp) & 3;
-    const int rh = (int(warp) >> 2) & 1;
-    const int hl = int(lane) >> 4;                        // key half of the row
-    const int row = wq * 32 + rh * 16 + (int(lane) & 15);  // row in the Q tile
-    const uint32_t lane_off = uint32_t(wq * 32 + rh * 16) << 16;
-    const uint32_t tS0 = tmem + lane_off + t * 128;
-    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
-    constexpr int kOHalf = D / 2;  // O columns per thread
-    const float sl2 = args.scale_log2;
-    const uint32_t obar = smem_u32(&bars->o_full[t]);
-    const bool tr = kTrace && trace != nullptr && (warp & 7) == 0 && lane == 0;
-    const int key0 = hl * 32;        // first key of my half of the tile
-    const int grow = q0 + t * kBM + row;
-    const int my_n_kv = t == 0 ? n0 : n1;
-
-    float m_run = -INFINITY;  // running max (scaled, log2 units), same in both halves
-    float l_run = 0.f;        // my half's partial normaliser relative to m_run
-
-    for (int j = 0; j < my_n_kv; ++j) {
-      const uint32_t tS = tS0 + (j & 1) * kBNX;
-      mbar_wait(smem_u32(&bars->s_full[t][j & 1]), uint32_t((j >> 1) & 1));
-      tc_fence_after();
-      if (tr) rec(kEvSm0SReady + 5 * t, j);
-      uint32_t sr[32];
-      tmem_ld_16x32bx2_x32<32>(tS, sr);
-      // last admitted key of the tile for this row (MaskSpec::admits,
-      // types.hpp:48-67): ragged tail / padding, causal diagonal
-      int lim = kBNX - 1;
-      if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBNX - 1);
-      if (args.mask == kMaskCausal) lim = min(lim, grow - j * kBNX);
-      const int llim = lim - key0;
-      tmem_wait_ld();
-      reg_fence(sr);
-      float s[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) s[i] = __uint_as_float(sr[i]);
-      if (__any_sync(0xffffffffu, llim < 31)) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i > llim) s[i] = -INFINITY;
-      }
-      if (tr) rec(kEvSm0Loaded + 5 * t, j);
-      float mx4[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) mx4[i] = s[i];
-#pragma unroll
-      for (int i = 4; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
-      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-      const float m_new = mx * sl2;
-      if (tr) rec(kEvSm0Max + 5 * t, j);
-      const bool need = m_new > m_run + kRescaleThreshold;
-      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
-      if (need) {
-        l_run *= alpha;
-        m_run = m_new;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // O holds PV(0..j-1): wait for PV(j-1), rescale in place (PV(j)
-        // waits for P(j), signalled below)
-        mbar_wait(obar, uint32_t((j - 1) & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < kOHalf / 16; ++c) {
-          uint32_t orow[16];
-          tmem_ld_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
-          tmem_wait_ld();
-          reg_fence(orow);
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
-          tmem_st_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
-        }
-      }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      const uint64_t sl2x2 = f2(sl2, sl2);
-      const uint64_t negm2 = f2(-m_use, -m_use);
-      uint64_t acc[2] = {0ull, 0ull};
-      uint32_t pk[16];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {  // groups of 8 columns
-        uint64_t x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          x[u] = ffma2(f2(s[g * 8 + 2 * u], s[g * 8 + 2 * u + 1]), sl2x2, negm2);
-        float p[8];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#ifdef TA_DEBUG_NO_EXP
-          if (true) {
-            f2_split(x[u], p[2 * u], p[2 * u + 1]);
-          } else
-#endif
-          if (2 * u >= 8 - kEmuPer8) {
-            ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
-          } else {
-            float a, b2;
-            f2_split(x[u], a, b2);
-            p[2 * u] = ex2(a);
-            p[2 * u + 1] = ex2(b2);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          acc[u & 1] = fadd2(acc[u & 1], f2(p[2 * u], p[2 * u + 1]));
-          pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
-        }
-      }
-      if (tr) rec(kEvSm0Exp + 5 * t, j);
-      // packed P of my 32 keys -> packed columns [0,16) / [32,48) of the buffer
-      tmem_st_16x32bx2_x16<32>(tS, pk);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t]));
-      {
-        float lo, hi;
-        f2_split(fadd2(acc[0], acc[1]), lo, hi);
-        l_run += lo + hi;
-      }
-      if (tr) rec(kEvSm0PArrive + 5 * t, j);
-    }
-
-    // ------------------------------------------------------------- epilogue
-    // (finalize, tiled.hpp:223-238): O = o / l, RNE to 16 bit; LSE = m + ln l;
-    // rows with no admitted key are zeros with LSE -inf
-    if (my_n_kv > 0) {
-      mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
-      tc_fence_after();
-    }
-    const float l_row = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
-    const float inv_l = l_row > 0.f ? 1.f / l_row : 0.f;
-    uint16_t* orow_g =
-        reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D + hl * kOHalf;
-#pragma unroll
-    for (int c = 0; c < kOHalf / 32; ++c) {
-      uint32_t orow[32];
-      if (my_n_kv > 0) {
-        tmem_ld_16x32bx2_x32<kOHalf>(tO + c * 32, orow);
-        tmem_wait_ld();
-        reg_fence(orow);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) orow[i] = 0u;
-      }
-      uint32_t packed[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
-                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
-      if (grow < S) {
-        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
-                              packed[4 * i + 3]);
-      }
-    }
-    if (args.lse != nullptr && grow < S && hl == 0)
-      args.lse[size_t(bh) * S + grow] =
-          l_row > 0.f ? (m_run + __log2f(l_row)) * kLn2 : -INFINITY;
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == kXWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
-}
-
-// ----------------------------------------------------------------------------
-// Variant "si" (self-issue): the ping-pong kernel with no MMA warp.  The
-// tensor-core work of a Q tile is issued by its own softmax warpgroup: the
-// last of the 4 warps to finish P part h (smem counter, acq_rel) issues
-// PV part h and, after the last part, S_t(j+1).  This removes the MMA warp's
-// mbarrier wake-up and its in-order coupling of the two tiles from the
-// critical loop S_t(j) -> softmax -> P -> PV_t(j) -> S_t(j+1).
-// ----------------------------------------------------------------------------
-constexpr int kThreadsSI = 384;  // warps 0-7 softmax (2 tiles x 4), 8 TMEM alloc, 9 TMA, 10-11 idle
-
-struct BarriersSI {
-  uint64_t q_full;
-  uint64_t s_full[kQTiles];
-  uint64_t o_full[kQTiles];
-  uint64_t slot_full[8];
-  uint64_t slot_empty[8];  // 2 arrivals: one per Q tile using the slot
-  uint32_t p_cnt[kQTiles][4];
-  uint32_t tmem_base;
-};
-
-__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t addr, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
-               : "=r"(old)
-               : "r"(addr), "r"(v)
-               : "memory");
-  return old;
-}
-
-template <int D, bool kBF16, bool kTrace>
-__global__ void __launch_bounds__(kThreadsSI, 1)
-    sdpa_fwd_si_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                       const __grid_constant__ CUtensorMap tmap_k,
-                       const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
-  using C = Cfg<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  const uint32_t sq = smem_u32(smem);
-  const uint32_t sring = sq + kQTiles * C::kTileBytes;
-  BarriersSI* bars = reinterpret_cast<BarriersSI*>(smem + C::kSmemData);
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();
-  const int S = args.seq_len;
-  const int bh = blockIdx.y;
-  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
-  const int q0 = qblk * (kBM * kQTiles);
-  const int kv_len =
-      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
-  const int n_kv_seq = (kv_len + kBN - 1) / kBN;
-  const int diag0 = q0 / kBN;
-  const int n0 = args.mask == kMaskCausal ? min(diag0 + 1, n_kv_seq) : n_kv_seq;
-  const int n1 = args.mask == kMaskCausal ? min(diag0 + 2, n_kv_seq) : n_kv_seq;
-  long long* const trace = (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
-  auto rec = [&](int ev, int j) {
-    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
-  };
-
-  if (threadIdx.x == kWarpTma * 32) {
-    mbar_init(smem_u32(&bars->q_full), 1);
-    for (int t = 0; t < kQTiles; ++t) {
-      mbar_init(smem_u32(&bars->s_full[t]), 1);
-      mbar_init(smem_u32(&bars->o_full[t]), 1);
-      for (int h = 0; h < 4; ++h) bars->p_cnt[t][h] = 0;
-    }
-    for (int s = 0; s < C::kSlots; ++s) {
-      mbar_init(smem_u32(&bars->slot_full[s]), 1);
-      mbar_init(smem_u32(&bars->slot_empty[s]), 2);
-    }
-    fence_barrier_init();
-  }
-  if (warp == kWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp >= kNumSoftmaxWarps) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
-    if (warp == kWarpTma && lane == 0 && n1 > 0) {
-      // ---------------------------------------------------------------- TMA
-      tma_prefetch_desc(&tmap_q);
-      tma_prefetch_desc(&tmap_k);
-      tma_prefetch_desc(&tmap_v);
-      const uint32_t qbar = smem_u32(&bars->q_full);
-      mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
-      for (int t = 0; t < kQTiles; ++t)
-        for (int r = 0; r < C::kRegions; ++r)
-          tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
-                      q0 + t * kBM, bh);
-      int slot = 0;
-      uint32_t phase = 0;
-      for (int j = 0; j < n1; ++j) {
-        for (int kv = 0; kv < 2; ++kv) {
-          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
-          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-          mbar_arrive_expect_tx(fbar, C::kTileBytes);
-          const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
-          for (int r = 0; r < C::kRegions; ++r)
-            tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
-                        j * kBN, bh);
-          if (++slot == C::kSlots) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else {
-    // -------------------------------------------------------------- softmax
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-    const int t = warp / 4;
-    const uint32_t wq = warp & 3;
-    const int row = int(wq * 32 + lane);
-    const uint32_t lane_off = (wq * 32u) << 16;
-    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN;
-    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
-    const float sl2 = args.scale_log2;
-    const uint32_t sbar = smem_u32(&bars->s_full[t]);
-    const uint32_t obar = smem_u32(&bars->o_full[t]);
-    const bool tr = kTrace && trace != nullptr && row == 0;
-    const int my_n = t == 0 ? n0 : n1;
-
-    // ---- tensor-core issue (one elected lane of the issuing warp)
-    constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
-    constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
-    // ring position r: K_j at 2j, V_j at 2j+1
-    auto slot_of = [](int r) { return r % C::kSlots; };
-    auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
-    // K_j / V_j are used by Q tile 0 only while j < n0: tile 1 releases for both after that
-    auto release = [&](int r) {
-      const uint32_t b = smem_u32(&bars->slot_empty[slot_of(r)]);
-      umma_commit_warp(b);
-      if (t == 1 && (r >> 1) >= n0) umma_commit_warp(b);
-    };
-    auto issue_qk = [&](int j) {
-      const int r = 2 * j;
-      mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
-      tc_fence_after();
-      uint64_t qd = sdesc_sw128(sq + t * C::kTileBytes, 16, 1024);
-      uint64_t kd = sdesc_sw128(sring + slot_of(r) * C::kTileBytes, 16, 1024);
-      asm volatile("" : "+l"(qd), "+l"(kd));
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
-        umma_ss_warp(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
-      }
-      umma_commit_warp(sbar);
-      release(r);
-    };
-    auto issue_pv_part = [&](int j, int h) {
-      const int r = 2 * j + 1;
-      if (h == 0) {
-        mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
-        tc_fence_after();
-      }
-      uint64_t vd = sdesc_sw128(sring + slot_of(r) * C::kTileBytes, C::kRegionBytes, 1024);
-      asm volatile("" : "+l"(vd));
-#pragma unroll
-      for (int kk = 0; kk < kBN / 16 / kPParts; ++kk) {
-        const int ks = h * (kBN / 16 / kPParts) + kk;
-        umma_ts_warp(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
-                     vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv, (j > 0 || ks > 0) ? 1u : 0u);
-      }
-      if (h == kPParts - 1) {
-        umma_commit_warp(obar);
-        release(r);
-      }
-    };
-
-    if (wq == 0 && my_n > 0) {  // S_t(0)
-      mbar_wait(smem_u32(&bars->q_full), 0);
-      tc_fence_after();
-      issue_qk(0);
-    }
-
-    float m_run = -INFINITY;  // running max used for the exponent (scaled, log2 units)
-    float l_run = 0.f;        // running normaliser relative to m_run
-
-    for (int j = 0; j < my_n; ++j) {
-      mbar_wait(sbar, uint32_t(j & 1));
-      tc_fence_after();
-      if (tr) rec(kEvSm0SReady + 5 * t, j);
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
-      int lim = kBN - 1;
-      if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
-      if (args.mask == kMaskCausal && j == diag0 + t) lim = min(lim, row);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
-      if (lim < kBN - 1) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (i > lim) s[i] = -INFINITY;
-      }
-      if (tr) rec(kEvSm0Loaded + 5 * t, j);
-      float mx8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
-#pragma unroll
-      for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float m_new = mx * sl2;
-      if (tr) rec(kEvSm0Max + 5 * t, j);
-      const bool need = m_new > m_run + kRescaleThreshold;
-      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
-      if (need) {
-        l_run *= alpha;
-        m_run = m_new;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // O holds PV(0..j-1): wait for PV(j-1), rescale in place (PV(j) is
-        // issued only after all 4 warps have written P part 0 below)
-        mbar_wait(obar, uint32_t((j - 1) & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t orow[32];
-          tmem_ld32(tO + c * 32, orow);
-          tmem_wait_ld();
-          reg_fence(orow);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
-          tmem_st32(tO + c * 32, orow);
-        }
-      }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      const uint64_t sl2x2 = f2(sl2, sl2);
-      const uint64_t negm2 = f2(-m_use, -m_use);
-      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-      for (int h = 0; h < kPParts; ++h) {
-        constexpr int kCols = kBN / kPParts;
-        uint32_t pk[kCols / 32][16];
-#pragma unroll
-        for (int g = 0; g < kCols / 8; ++g) {
-          const int c0 = h * kCols + g * 8;
-          uint64_t x[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
-          float p[8];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-#ifdef TA_DEBUG_NO_EXP
-            if (true) {
-              f2_split(x[u], p[2 * u], p[2 * u + 1]);
-            } else
-#endif
-            if (2 * u >= 8 - kEmuPer8) {
-              ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
-            } else {
-              float a, b;
-              f2_split(x[u], a, b);
-              p[2 * u] = ex2(a);
-              p[2 * u + 1] = ex2(b);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
-            pk[(g * 4 + u) / 16][(g * 4 + u) % 16] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < kCols / 32; ++i) tmem_st16(tS + h * (kCols / 2) + i * 16, pk[i]);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        // the last of the tile's 4 warps to land P part h issues PV part h
-        uint32_t last = 0;
-        if (lane == 0) {
-          const uint32_t cnt = smem_u32(&bars->p_cnt[t][h]);
-          last = atom_add_acq_rel(cnt, 1u) == 3u;
-          if (last) st_shared_relaxed(cnt, 0u);
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-          tc_fence_after();
-          issue_pv_part(j, h);
-          if (h == kPParts - 1 && j + 1 < my_n) issue_qk(j + 1);
-          if (h == kPParts - 1 && tr) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
-        }
-        if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
-      }
-      {
-        const uint64_t a01 = fadd2(acc[0], acc[1]);
-        const uint64_t a23 = fadd2(acc[2], acc[3]);
-        float lo, hi;
-        f2_split(fadd2(a01, a23), lo, hi);
-        l_run += lo + hi;
-      }
-      if (tr) rec(kEvSm0PArrive + 5 * t, j);
-    }
-
-    // ------------------------------------------------------------- epilogue
-    if (my_n > 0) {
-      mbar_wait(obar, uint32_t((my_n - 1) & 1));
-      tc_fence_after();
-    }
-    const int grow = q0 + t * kBM + row;
-    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t orow[32];
-      if (my_n > 0) {
-        tmem_ld32(tO + c * 32, orow);
-        tmem_wait_ld();
-        reg_fence(orow);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) orow[i] = 0u;
-      }
-      uint32_t packed[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
-                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
-      if (grow < S) {
-        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
-                              packed[4 * i + 3]);
-      }
-    }
-    if (args.lse != nullptr && grow < S)
-      args.lse[size_t(bh) * S + grow] =
-          l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == kWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
-}
-
-template <int D, bool kBF16>
-cudaError_t launch_si(const FwdLaunch& L) {
-  using C = Cfg<D>;
-  auto kern = L.args.trace != nullptr ? sdpa_fwd_si_kernel<D, kBF16, true>
-                                      : sdpa_fwd_si_kernel<D, kBF16, false>;
-  static bool attr_set[64][2] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int tr = L.args.trace != nullptr;
-  if (dev < 64 && !attr_set[dev][tr]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set[dev][tr] = true;
-  }
-  const int rows_per_cta = kBM * kQTiles;
-  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
-  kern<<<grid, kThreadsSI, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
-      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
-  return cudaGetLastError();
-}
-
-// ----------------------------------------------------------------------------
-// Variant "db": one 128-row Q tile per CTA with double-buffered S in TMEM.
-// The tensor core computes S(j+1) while the softmax of S(j) runs and then
-// PV(j); the softmax runs back to back against a 1024-cycle MMA budget per
-// K/V tile (D=128) instead of racing the other Q tile of a ping-pong pair.
-// ----------------------------------------------------------------------------
-constexpr int kThreadsDB = 256;  // warps 0-3 softmax, 4 TMEM alloc, 5 TMA, 7 MMA
-constexpr int kDBWarpAlloc = 4, kDBWarpTma = 5, kDBWarpMma = 7;
-
-template <int D>
-struct CfgDB {
-  static constexpr int kRegions = D / 64;
-  static constexpr int kTileBytes = kBM * D * 2;
-  static constexpr int kRegionBytes = kBM * 128;
-  static constexpr int kSlots = D == 128 ? 6 : 12;
-  static constexpr int kSmemData = kTileBytes + kSlots * kTileBytes;
-  static constexpr int kSmemBytes = kSmemData + 1024 + 1024;
-  static constexpr uint32_t kTmemS = 0;    // S buffers at cols 0 and 128
-  static constexpr uint32_t kTmemO = 256;  // O at 256 .. 256 + D
-};
-
-struct BarriersDB {
-  uint64_t q_full;
-  uint64_t s_full[2];   // per S buffer
-  uint64_t p_full[2];   // P halves (keys [0,64) / [64,128)) of the current tile
-  uint64_t o_full;      // PV(j) complete
-  uint64_t slot_full[12];
-  uint64_t slot_empty[12];
-  uint32_t tmem_base;
-};
-
-template <int D, bool kBF16>
-__global__ void __launch_bounds__(kThreadsDB, 1)
-    sdpa_fwd_db_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                       const __grid_constant__ CUtensorMap tmap_k,
-                       const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
-  using C = CfgDB<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  const uint32_t sq = smem_u32(smem);
-  const uint32_t sring = sq + C::kTileBytes;
-  BarriersDB* bars = reinterpret_cast<BarriersDB*>(smem + C::kSmemData);
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();
-  const int S = args.seq_len;
-  const int bh = blockIdx.y;
-  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
-  const int q0 = qblk * kBM;
-  const int kv_len =
-      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
-  const int n_kv_seq = (kv_len + kBN - 1) / kBN;
-  const int diag = q0 / kBN;  // causal: the K/V tile on this Q tile's diagonal
-  const int n_kv = args.mask == kMaskCausal ? min(diag + 1, n_kv_seq) : n_kv_seq;
-  long long* const trace =
-      (args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
-  auto rec = [&](int ev, int j) {
-    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
-  };
-  // K/V ring order = MMA consumption order: K0, K1, V0, K2, V1, K3, V2, ...
-  // (S(j+2) is issued right after PV(j)).
-
-  if (threadIdx.x == kDBWarpTma * 32) {
-    mbar_init(smem_u32(&bars->q_full), 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&bars->s_full[b]), 1);
-      mbar_init(smem_u32(&bars->p_full[b]), kBM / 32);
-    }
-    mbar_init(smem_u32(&bars->o_full), 1);
-    for (int s = 0; s < C::kSlots; ++s) {
-      mbar_init(smem_u32(&bars->slot_full[s]), 1);
-      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == kDBWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  // the consumption sequence as (tile, is_v) pairs, generated in order:
-  // K0, [K1], then for i = 0..n-1: V_i, [K_{i+2}]
-  if (warp == kDBWarpTma) {
-    // ------------------------------------------------------------------ TMA
-    if (lane == 0 && n_kv > 0) {
-      tma_prefetch_desc(&tmap_q);
-      tma_prefetch_desc(&tmap_k);
-      tma_prefetch_desc(&tmap_v);
-      const uint32_t qbar = smem_u32(&bars->q_full);
-      mbar_arrive_expect_tx(qbar, C::kTileBytes);
-      for (int r = 0; r < C::kRegions; ++r)
-        tma_load_3d(sq + r * C::kRegionBytes, &tmap_q, qbar, r * 64, q0, bh);
-      int slot = 0;
-      uint32_t phase = 0;
-      auto load = [&](const CUtensorMap* map, int tile) {
-        mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
-        const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-        mbar_arrive_expect_tx(fbar, C::kTileBytes);
-        for (int r = 0; r < C::kRegions; ++r)
-          tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
-                      tile * kBN, bh);
-        if (++slot == C::kSlots) {
-          slot = 0;
-          phase ^= 1;
-        }
-      };
-      load(&tmap_k, 0);
-      if (n_kv > 1) load(&tmap_k, 1);
-      for (int i = 0; i < n_kv; ++i) {
-        load(&tmap_v, i);
-        if (i + 2 < n_kv) load(&tmap_k, i + 2);
-      }
-    }
-    __syncwarp();
-  } else if (warp == kDBWarpMma) {
-    // ------------------------------------------------------------------ MMA
-    constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
-    constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
-    int pos = 0;  // position in the ring sequence
-    auto slot_of = [](int r) { return r % C::kSlots; };
-    auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
-    auto wait_full = [&](int r) {
-      mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
-      tc_fence_after();
-    };
-    auto release = [&](int r) { umma_commit_warp(smem_u32(&bars->slot_empty[slot_of(r)])); };
-    const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
-    const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
-    const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
-    auto issue_qk = [&](int buf, int r) {
-      uint64_t qd = qdesc;
-      uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-      asm volatile("" : "+l"(qd), "+l"(kd));
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
-        umma_ss_warp(tmem + C::kTmemS + buf * kBN, qd + off, kd + off, idesc_qk, ks > 0);
-      }
-      umma_commit_warp(smem_u32(&bars->s_full[buf]));
-    };
-    auto issue_pv = [&](int buf, int r, bool accumulate, int j) {
-      uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-      asm volatile("" : "+l"(vd));
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        mbar_wait(smem_u32(&bars->p_full[h]), uint32_t(j & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < kBN / 32; ++kk) {
-          const int ks = h * (kBN / 32) + kk;
-          umma_ts_warp(tmem + C::kTmemO, tmem + C::kTmemS + buf * kBN + ks * 8,
-                       vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
-                       (accumulate || ks > 0) ? 1u : 0u);
-        }
-      }
-      umma_commit_warp(smem_u32(&bars->o_full));
-    };
-    if (n_kv > 0) {
-      mbar_wait(smem_u32(&bars->q_full), 0);
-      tc_fence_after();
-      wait_full(pos);
-      issue_qk(0, pos);
-      release(pos++);
-      if (n_kv > 1) {
-        wait_full(pos);
-        issue_qk(1, pos);
-        release(pos++);
-      }
-      for (int j = 0; j < n_kv; ++j) {
-        wait_full(pos);
-        if (lane == 0) rec(kEvMmaWaitP0, j);
-        issue_pv(j & 1, pos, j > 0, j);
-        release(pos++);
-        if (lane == 0) rec(kEvMmaIssuedPV0, j);
-        if (j + 2 < n_kv) {
-          wait_full(pos);
-          issue_qk(j & 1, pos);  // S(j+2) reuses the buffer PV(j) just read
-          release(pos++);
-        }
-      }
-    }
-  } else if (warp < 4) {
-    // -------------------------------------------------------------- softmax
-    const uint32_t wq = warp & 3;
-    const int row = int(wq * 32 + lane);
-    const uint32_t lane_off = (wq * 32u) << 16;
-    const uint32_t tO = tmem + lane_off + C::kTmemO;
-    const float sl2 = args.scale_log2;
-    const uint32_t obar = smem_u32(&bars->o_full);
-    float m_run = -INFINITY;
-    float l_run = 0.f;
-    const uint64_t sl2x2 = f2(sl2, sl2);
-    const bool tr = (row == 0);
-
-    for (int j = 0; j < n_kv; ++j) {
-      const int buf = j & 1;
-      const uint32_t tS = tmem + lane_off + C::kTmemS + buf * kBN;
-      mbar_wait(smem_u32(&bars->s_full[buf]), uint32_t((j >> 1) & 1));
-      tc_fence_after();
-      if (tr) rec(kEvSm0SReady, j);
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
-      if (tr) rec(kEvSm0Loaded, j);
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
-      {
-        int lim = kBN - 1;
-        if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
-        if (args.mask == kMaskCausal && j == diag) lim = min(lim, row);
-        if (lim < kBN - 1) {
-#pragma unroll
-          for (int i = 0; i < 128; ++i)
-            if (i > lim) s[i] = -INFINITY;
-        }
-      }
-      float mx8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
-#pragma unroll
-      for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float m_new = mx * sl2;
-      if (tr) rec(kEvSm0Max, j);
-      const bool need = m_new > m_run + kRescaleThreshold;
-      const float alpha = need ? ex2(m_run - m_new) : 1.f;
-      if (need) {
-        l_run *= alpha;
-        m_run = m_new;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // O holds PV(0..j-1); wait for PV(j-1), rescale in place (PV(j) waits
-        // for P(j), signalled below)
-        mbar_wait(obar, uint32_t((j - 1) & 1));
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t orow[32];
-          tmem_ld32(tO + c * 32, orow);
-          tmem_wait_ld();
-          reg_fence(orow);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
-          tmem_st32(tO + c * 32, orow);
-        }
-      }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      const uint64_t negm2 = f2(-m_use, -m_use);
-      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t pk[32];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const int c0 = h * 64 + g * 8;
-          uint64_t x[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
-          float p[8];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-#ifdef TA_DEBUG_NO_EXP
-            if (true) {
-              f2_split(x[u], p[2 * u], p[2 * u + 1]);
-            } else
-#endif
-            if (2 * u >= 8 - kEmuPer8) {
-              ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
-            } else {
-              float a, b;
-              f2_split(x[u], a, b);
-              p[2 * u] = ex2(a);
-              p[2 * u + 1] = ex2(b);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
-            pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
-          }
-        }
-        tmem_st32(tS + h * 32, pk);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[h]));
-        if (h == 0 && tr) rec(kEvSm0Exp, j);
-      }
-      {
-        const uint64_t a01 = fadd2(acc[0], acc[1]);
-        const uint64_t a23 = fadd2(acc[2], acc[3]);
-        float lo, hi;
-        f2_split(fadd2(a01, a23), lo, hi);
-        l_run += lo + hi;
-      }
-      if (tr) rec(kEvSm0PArrive, j);
-    }
-
-    // ------------------------------------------------------------- epilogue
-    if (n_kv > 0) {
-      mbar_wait(obar, uint32_t((n_kv - 1) & 1));
-      tc_fence_after();
-    }
-    const int grow = q0 + row;
-    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t orow[32];
-      if (n_kv > 0) {
-        tmem_ld32(tO + c * 32, orow);
-        tmem_wait_ld();
-        reg_fence(orow);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) orow[i] = 0u;
-      }
-      uint32_t packed[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
-                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
-      if (grow < S) {
-        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
-                              packed[4 * i + 3]);
-      }
-    }
-    if (args.lse != nullptr && grow < S)
-      args.lse[size_t(bh) * S + grow] =
-          l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == kDBWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
-}
-
-// ----------------------------------------------------------------------------
 // Descriptor self-test: one 128x128x128 UMMA product, checked on the host.
 //   mode 0: D = A * B^T, A [128][128] K-major, B [128 n][128 k] K-major (QK^T)
 //   mode 1: D = A * B,   A K-major, B [128 k][128 n] MN-major       (PV, SS)
@@ -2012,25 +1038,6 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 template <int D, bool kBF16>
-cudaError_t launch_db(const FwdLaunch& L) {
-  using C = CfgDB<D>;
-  auto kern = sdpa_fwd_db_kernel<D, kBF16>;
-  static bool attr_set[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !attr_set[dev]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set[dev] = true;
-  }
-  dim3 grid((L.args.seq_len + kBM - 1) / kBM, L.bh);
-  kern<<<grid, kThreadsDB, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
-      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
-  return cudaGetLastError();
-}
-
-template <int D, bool kBF16>
 cudaError_t launch_rs(const FwdLaunch& L) {
   using C = Cfg<D>;
   auto kern = L.args.trace != nullptr ? sdpa_fwd_rs_kernel<D, kBF16, true>
@@ -2053,11 +1060,12 @@ cudaError_t launch_rs(const FwdLaunch& L) {
 }
 
 template <int D, bool kBF16>
-cudaError_t launch_x(const FwdLaunch& L) {
-  using C = CfgX<D>;
-  auto kern = L.args.trace != nullptr ? sdpa_fwd_x_kernel<D, kBF16, true>
-                                      : sdpa_fwd_x_kernel<D, kBF16, false>;
-  static bool attr_set[64][2] = {};
+cudaError_t launch_typed(const FwdLaunch& L) {
+  if (L.variant == 2) return launch_rs<D, kBF16>(L);
+  using C = Cfg<D>;
+  auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true>
+                                      : sdpa_fwd_kernel<D, kBF16, false>;
+  static bool attr_set[64][2] = {};  // per device, per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
   const int tr = L.args.trace != nullptr;
@@ -2066,30 +1074,6 @@ cudaError_t launch_x(const FwdLaunch& L) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set[dev][tr] = true;
-  }
-  const int rows_per_cta = kBM * kQTiles;
-  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
-  kern<<<grid, kThreadsX, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
-      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
-  return cudaGetLastError();
-}
-
-template <int D, bool kBF16>
-cudaError_t launch_typed(const FwdLaunch& L) {
-  if (L.variant == 4) return launch_si<D, kBF16>(L);
-  if (L.variant == 3) return launch_x<D, kBF16>(L);
-  if (L.variant == 1) return launch_db<D, kBF16>(L);
-  if (L.variant == 2) return launch_rs<D, kBF16>(L);
-  using C = Cfg<D>;
-  auto kern = sdpa_fwd_kernel<D, kBF16>;
-  static bool attr_set[64] = {};  // per device
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !attr_set[dev]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set[dev] = true;
   }
   const int rows_per_cta = kBM * kQTiles;
   dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
@@ -2103,16 +1087,14 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 FwdGeometry fwd_geometry(int64_t S, int64_t BH, int variant) {
   FwdGeometry g;
   g.block_m = kBM;
-  g.block_n = variant == 3 ? kBNX : kBN;
-  g.q_tiles_per_cta = variant == 1 ? 1 : kQTiles;
-  g.threads = variant == 1 ? kThreadsDB : variant == 2 ? kThreadsRS : variant == 3 ? kThreadsX : kThreads;
+  g.block_n = kBN;
+  g.q_tiles_per_cta = kQTiles;
+  g.threads = variant == 2 ? kThreadsRS : kThreads;
   g.ctas = ((S + kBM * g.q_tiles_per_cta - 1) / (kBM * g.q_tiles_per_cta)) * BH;
   return g;
 }
 
 int fwd_ring_slots(int D, int variant) {
-  if (variant == 3) return D == 128 ? CfgX<128>::kSlots : CfgX<64>::kSlots;
-  if (variant == 1) return D == 128 ? CfgDB<128>::kSlots : CfgDB<64>::kSlots;
   return D == 128 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
 }
 

@@ -49,6 +49,9 @@ enum TraceEvent {
   kEvTcS0Done,   // s_full[0] phase j+1 completed (S0(j+1) done)
   kEvTcPV1Done,
   kEvTcS1Done,
+  kEvSm0ArriveW1,  // Q tile 0, warps 1..3: last P part arrived (warp skew)
+  kEvSm0ArriveW2,
+  kEvSm0ArriveW3,
   kNumTraceEvents
 };
 

@@ -11,12 +11,12 @@ q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=torch.bfloat16) for _ in
 o = torch.empty_like(q)
 for _ in range(3):
     ta.sdpa(q, k, v, out=o)
-tr = torch.zeros(18 * 64, dtype=torch.int64, device="cuda")
+tr = torch.zeros(24 * 64, dtype=torch.int64, device="cuda")
 L = ta.lib()
 L.ta_debug_sdpa_trace.restype = ctypes.c_int
 L.ta_debug_sdpa_trace.argtypes = [ctypes.c_void_p] * 4 + [ta._Shape, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
 ta._check(L.ta_debug_sdpa_trace(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), ta._Shape(B, H, S, D), ta.BF16, tr.data_ptr(), None))
-t = tr.view(18, 64).cpu().numpy()
+t = tr.view(24, 64).cpu().numpy()
 names = ["mmaWaitP0", "mmaIssPV0", "mmaWaitP1", "mmaIssPV1", "s0Ready", "s0Load", "s0Max", "s0Exp", "s0Arrive", "s1Ready", "s1Load", "s1Max", "s1Exp", "s1Arrive", "tcPV0", "tcS0", "tcPV1", "tcS1"]
 base = t[4, 0]
 n = min(64, (S + 127) // 128)
@@ -30,6 +30,7 @@ print("mean over iters 8..n-2 (cycles):")
 print(" period s0Ready->s0Ready", np.mean([t[4, j + 1] - t[4, j] for j in js]))
 print(" s0: ready->load %.0f load->max %.0f max->exp %.0f exp->arrive %.0f" % (d(4, 5), d(5, 6), d(6, 7), d(7, 8)))
 print(" s1: ready->load %.0f load->max %.0f max->exp %.0f exp->arrive %.0f" % (d(9, 10), d(10, 11), d(11, 12), d(12, 13)))
+print(" tile-0 warp skew (warp w arrive - warp 0 arrive) w=1,2,3:", [np.mean([t[17 + w, j] - t[8, j] for j in js]) for w in (1, 2, 3)])
 print(" s0 arrive(j) -> mma sees P0(j):", np.mean([t[0, j] - t[8, j] for j in js]))
 print(" mma saw P0(j) -> PV0(j) issued:", np.mean([t[1, j] - t[0, j] for j in js]))
 print(" s1 arrive(j) -> mma sees P1(j):", np.mean([t[2, j] - t[13, j] for j in js]))
