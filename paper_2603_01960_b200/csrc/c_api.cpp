@@ -101,21 +101,8 @@ ta_status validate_device_support(ta_shape sh, ta_dtype dt, ta_mask_kind mask) {
 // (t_m, t_n, D, dtype, causal).  The plan records the executed GPU tiling.
 // ---------------------------------------------------------------------------
 struct Plan {
-  int block_m, block_n, stages, q_tiles, threads, variant;
+  int block_m, block_n, stages, q_tiles, threads;
 };
-
-// Kernel variant: TA_DEFAULT_VARIANT at build time; TILEATTN_B200_VARIANT
-// (0 = ping-pong, 1 = double-buffered S) overrides it for A/B measurements.
-#ifndef TA_DEFAULT_VARIANT
-#define TA_DEFAULT_VARIANT 0
-#endif
-int kernel_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("TILEATTN_B200_VARIANT");
-    return e ? std::atoi(e) : TA_DEFAULT_VARIANT;
-  }();
-  return v;
-}
 
 struct PlanCache {
   std::mutex mu;
@@ -139,11 +126,9 @@ std::shared_ptr<const Plan> get_plan(const ta_schedule& s, int64_t d, ta_dtype d
       return it->second;
     }
   }
-  const int variant = kernel_variant();
-  auto g = ta::fwd_geometry(1, 1, variant);
-  auto plan = std::make_shared<const Plan>(Plan{g.block_m, g.block_n,
-                                                ta::fwd_ring_slots(int(d), variant),
-                                                g.q_tiles_per_cta, g.threads, variant});
+  auto g = ta::fwd_geometry(1, 1);
+  auto plan = std::make_shared<const Plan>(
+      Plan{g.block_m, g.block_n, ta::fwd_ring_slots(int(d)), g.q_tiles_per_cta, g.threads});
   c.constructions.fetch_add(1, std::memory_order_relaxed);
   std::lock_guard<std::mutex> lock(c.mu);
   auto [it, inserted] = c.plans.emplace(key, std::move(plan));
@@ -229,7 +214,7 @@ void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh, ta_mask_kind ma
   const int64_t bh = sh.b * sh.h;
   const int64_t q_tiles = (sh.s + p.block_m - 1) / p.block_m;
   const int64_t kv_tiles = (sh.s + p.block_n - 1) / p.block_n;
-  const auto g = ta::fwd_geometry(sh.s, bh, p.variant);
+  const auto g = ta::fwd_geometry(sh.s, bh);
   uint64_t visited = 0;
   if (mask == TA_MASK_CAUSAL) {
     for (int64_t qt = 0; qt < q_tiles; ++qt) {
@@ -290,7 +275,6 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.bh = bh;
   L.head_dim = int(sh.d);
   L.bf16 = bf16;
-  L.variant = plan.variant;
   L.stream = stream;
 
   cudaError_t e = ta::launch_sdpa_fwd(L);

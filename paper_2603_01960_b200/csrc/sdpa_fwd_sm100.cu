@@ -581,375 +581,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ----------------------------------------------------------------------------
-// Variant "rs" (row split): the ping-pong kernel above with 16 softmax warps,
-// two per TMEM lane quadrant per Q tile.  Warp w (t = w / 8, rh = (w / 4) & 1,
-// quadrant q = w & 3) owns rows q*32 + rh*16 + [0, 16); with the 16x32bx2
-// TMEM shape lane l holds row (l & 15) and key half l >> 4 (64 columns), so a
-// row's max / sum is one xor-16 shuffle.  Each SMSP then runs two softmax
-// warps per Q tile: the latency of one tile's softmax is about halved, which
-// is what the 2-tile ping-pong needs (softmax(t) must fit under the MMAs of
-// the other tile, ~1024 cycles at D=128).
-// ----------------------------------------------------------------------------
-constexpr int kThreadsRS = 640;  // 20 warps: 16 softmax + TMEM alloc, TMA, spare, MMA
-constexpr int kRSWarpAlloc = 16, kRSWarpTma = 17, kRSWarpMma = 19;
-// Registers are allocated per SMSP (warp w lives on SMSP w % 4): 5 warps per
-// SMSP cap the launch allocation at 96; setmaxnreg moves 64 from each control
-// thread to the softmax threads (4 x 32 x 112 + 32 x 32 = 15360 <= 16384).
-constexpr int kRSLaunchRegs = 96;
-constexpr int kRSRegsControl = 32;
-constexpr int kRSRegsSoftmax = 112;
-static_assert(16 * 32 * (kRSRegsSoftmax - kRSLaunchRegs) <=
-                  4 * 32 * (kRSLaunchRegs - kRSRegsControl),
-              "setmaxnreg.inc would wait forever: register pool does not balance");
-
-template <int D, bool kBF16, bool kTrace>
-__global__ void __launch_bounds__(kThreadsRS, 1)
-    sdpa_fwd_rs_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                       const __grid_constant__ CUtensorMap tmap_k,
-                       const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
-  using C = Cfg<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  const uint32_t sq = smem_u32(smem);
-  const uint32_t sring = sq + kQTiles * C::kTileBytes;
-  Barriers* bars = reinterpret_cast<Barriers*>(smem + C::kSmemData);
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();
-  const int S = args.seq_len;
-  const int bh = blockIdx.y;
-  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
-  const int q0 = qblk * (kBM * kQTiles);
-  const int kv_len =
-      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
-  const int n_kv_seq = (kv_len + kBN - 1) / kBN;
-  const int diag0 = q0 / kBN;
-  int n_kv_t[kQTiles];
-#pragma unroll
-  for (int t = 0; t < kQTiles; ++t)
-    n_kv_t[t] = args.mask == kMaskCausal ? min(diag0 + t + 1, n_kv_seq) : n_kv_seq;
-  const int n_kv = n_kv_t[kQTiles - 1];
-  long long* const trace =
-      (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
-  auto rec = [&](int ev, int j) {
-    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
-  };
-
-  if (threadIdx.x == kRSWarpMma * 32) {
-    mbar_init(smem_u32(&bars->q_full), 1);
-    for (int t = 0; t < kQTiles; ++t) {
-      mbar_init(smem_u32(&bars->s_full[t]), 1);
-      for (int q = 0; q < 2; ++q) mbar_init(smem_u32(&bars->p_full[t][q]), 8);  // 8 warps/tile
-      mbar_init(smem_u32(&bars->o_full[t]), 1);
-    }
-    for (int s = 0; s < C::kSlots; ++s) {
-      mbar_init(smem_u32(&bars->slot_full[s]), 1);
-      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == kRSWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp >= 16) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRSRegsControl));
-  if (warp == kRSWarpTma) {
-    // ------------------------------------------------------------------ TMA
-    if (lane == 0) {
-      tma_prefetch_desc(&tmap_q);
-      tma_prefetch_desc(&tmap_k);
-      tma_prefetch_desc(&tmap_v);
-      const uint32_t qbar = smem_u32(&bars->q_full);
-      if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
-      for (int t = 0; t < kQTiles && n_kv > 0; ++t)
-        for (int r = 0; r < C::kRegions; ++r)
-          tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
-                      q0 + t * kBM, bh);
-      int slot = 0;
-      uint32_t phase = 0;
-      for (int j = 0; j < n_kv; ++j) {
-        for (int kv = 0; kv < 2; ++kv) {
-          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
-          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-          mbar_arrive_expect_tx(fbar, C::kTileBytes);
-          const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
-          for (int r = 0; r < C::kRegions; ++r)
-            tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
-                        j * kBN, bh);
-          if (++slot == C::kSlots) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == kRSWarpMma) {
-    // ------------------------------------------------------------------ MMA
-    // Register-lean (32 registers after setmaxnreg): barrier addresses are
-    // re-derived from an opaque base at each use instead of being hoisted.
-    constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
-    constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
-    const uint32_t bb = smem_u32(bars);
-    auto bar = [&](uint32_t off) { return opaque(bb) + off; };
-    auto slot_of = [](int r) { return r % C::kSlots; };
-    auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
-    auto wait_full = [&](int r) {
-      mbar_wait(bar(offsetof(Barriers, slot_full) + 8 * slot_of(r)), phase_of(r));
-      tc_fence_after();
-    };
-    auto release = [&](int r) {
-      umma_commit_warp(bar(offsetof(Barriers, slot_empty) + 8 * slot_of(r)));
-    };
-    const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
-    const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
-    const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
-    auto issue_qk = [&](int t, int r) {
-      uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
-      uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-      asm volatile("" : "+l"(qd), "+l"(kd));
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
-        umma_ss_warp(opaque(tmem) + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
-      }
-      umma_commit_warp(bar(offsetof(Barriers, s_full) + 8 * t));
-    };
-    // P of key k sits in packed column k / 2; part h = K-steps {2h, 2h+1,
-    // 4+2h, 5+2h} (keys [32h, 32h+32) of each key half of the rows).
-    auto issue_pv = [&](int t, int r, bool accumulate, int j) {
-      uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-      asm volatile("" : "+l"(vd));
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        mbar_wait(bar(offsetof(Barriers, p_full) + 8 * (4 * t + h)), uint32_t(j & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int ks = (kk >> 1) * 4 + 2 * h + (kk & 1);
-          umma_ts_warp(opaque(tmem) + C::kTmemO + t * D, opaque(tmem) + C::kTmemS + t * kBN + ks * 8,
-                       vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
-                       (accumulate || h > 0 || kk > 0) ? 1u : 0u);
-        }
-      }
-      umma_commit_warp(bar(offsetof(Barriers, o_full) + 8 * t));
-    };
-    const int n0 = n_kv_t[0], n1 = n_kv_t[1];
-    if (n1 > 0) {
-      mbar_wait(smem_u32(&bars->q_full), 0);
-      tc_fence_after();
-      wait_full(0);
-      if (n0 > 0) issue_qk(0, 0);
-      issue_qk(1, 0);
-      release(0);
-      for (int j = 1; j < n1; ++j) {
-        const int rk = 2 * j, rv = 2 * j - 1;
-        wait_full(rv);
-        if (j - 1 < n0) issue_pv(0, rv, j > 1, j - 1);
-        wait_full(rk);
-        if (j < n0) issue_qk(0, rk);
-        issue_pv(1, rv, j > 1, j - 1);
-        release(rv);
-        issue_qk(1, rk);
-        release(rk);
-      }
-      const int rv = 2 * n1 - 1;
-      wait_full(rv);
-      if (n1 - 1 < n0) issue_pv(0, rv, n1 > 1, n1 - 1);
-      issue_pv(1, rv, n1 > 1, n1 - 1);
-      release(rv);
-    }
-  }
-  } else {
-    // -------------------------------------------------------------- softmax
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRSRegsSoftmax));
-    const int t = int(warp) >> 3;
-    const int wq = int(warp) & 3;
-    const int rh = (int(warp) >> 2) & 1;
-    const int hl = int(lane) >> 4;                        // key half of the row
-    const int row = wq * 32 + rh * 16 + (int(lane) & 15);  // row in the Q tile
-    const uint32_t lane_off = uint32_t(wq * 32 + rh * 16) << 16;
-    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN;
-    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
-    constexpr int kOHalf = D / 2;  // O columns per thread
-    const float sl2 = args.scale_log2;
-    const uint32_t sbar = smem_u32(&bars->s_full[t]);
-    const uint32_t obar = smem_u32(&bars->o_full[t]);
-    const bool tr = kTrace && trace != nullptr && (warp & 7) == 0 && lane == 0;
-    const int key0 = hl * 64;  // first key of my column half
-
-    float m_run = -INFINITY;  // running max (scaled, log2 units), same in both halves
-    float l_run = 0.f;        // my half's partial normaliser relative to m_run
-
-    // P layout: the 16-bit P of my key half goes to packed columns
-    // [32 hl, 32 hl + 32) of the S tile (key k -> column k / 2); both halves
-    // of a row are read (tcgen05.wait::ld) before either writes.  P is handed
-    // to the MMA in two parts: part h = keys [32h, 32h+32) + [64+32h, 96+32h).
-    const int my_n_kv = n_kv_t[t];
-    for (int j = 0; j < my_n_kv; ++j) {
-      mbar_wait(sbar, uint32_t(j & 1));
-      tc_fence_after();
-      if (tr) rec(kEvSm0SReady + 5 * t, j);
-      uint32_t sr[2][32];
-      tmem_ld_16x32bx2_x32<64>(tS, sr[0]);
-      tmem_ld_16x32bx2_x32<64>(tS + 32, sr[1]);
-      int lim = kBN - 1;
-      if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
-      if (args.mask == kMaskCausal && j == diag0 + t) lim = min(lim, row);
-      const int llim = lim - key0;  // last admitted local column
-      tmem_wait_ld();
-      reg_fence(sr[0]);
-      reg_fence(sr[1]);
-      float s[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
-      if (__any_sync(0xffffffffu, llim < 63)) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (i > llim) s[i] = -INFINITY;
-      }
-      if (tr) rec(kEvSm0Loaded + 5 * t, j);
-      float mx8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
-#pragma unroll
-      for (int i = 8; i < 64; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-      const float m_new = mx * sl2;
-      if (tr) rec(kEvSm0Max + 5 * t, j);
-      const bool need = m_new > m_run + kRescaleThreshold;
-      const float alpha = need ? ex2(m_run - m_new) : 1.f;  // 0 on the first tile
-      if (need) {
-        l_run *= alpha;
-        m_run = m_new;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // O holds PV(0..j-1): wait for PV(j-1), rescale in place (PV(j)
-        // waits for P(j), signalled below)
-        mbar_wait(obar, uint32_t((j - 1) & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < kOHalf / 16; ++c) {
-          uint32_t orow[16];
-          tmem_ld_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
-          tmem_wait_ld();
-          reg_fence(orow);
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
-          tmem_st_16x32bx2_x16<kOHalf>(tO + c * 16, orow);
-        }
-      }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      const uint64_t sl2x2 = f2(sl2, sl2);
-      const uint64_t negm2 = f2(-m_use, -m_use);
-      uint64_t acc[2] = {0ull, 0ull};
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int qq = 0; qq < 2; ++qq) {  // 16 columns -> 8 packed P words
-          uint32_t pk[8];
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {  // groups of 8 columns
-            const int c0 = h * 32 + qq * 16 + g * 8;
-            uint64_t x[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
-            float p[8];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-#ifdef TA_DEBUG_NO_EXP
-              if (true) {
-                f2_split(x[u], p[2 * u], p[2 * u + 1]);
-              } else
-#endif
-              if (2 * u >= 8 - kEmuPer8) {
-                ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
-              } else {
-                float a, b2;
-                f2_split(x[u], a, b2);
-                p[2 * u] = ex2(a);
-                p[2 * u + 1] = ex2(b2);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              acc[u & 1] = fadd2(acc[u & 1], f2(p[2 * u], p[2 * u + 1]));
-              pk[g * 4 + u] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
-            }
-          }
-          // keys key0 + 32h + 16qq + [0, 16) -> packed columns 32 hl + 16h + 8qq + [0, 8)
-          tmem_st_16x32bx2_x8<32>(tS + h * 16 + qq * 8, pk);
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
-        if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
-      }
-      {
-        float lo, hi;
-        f2_split(fadd2(acc[0], acc[1]), lo, hi);
-        l_run += lo + hi;
-      }
-      if (tr) rec(kEvSm0PArrive + 5 * t, j);
-    }
-
-    // ------------------------------------------------------------- epilogue
-    if (my_n_kv > 0) {
-      mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
-      tc_fence_after();
-    }
-    const float l_row = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
-    const int grow = q0 + t * kBM + row;
-    const float inv_l = l_row > 0.f ? 1.f / l_row : 0.f;
-    uint16_t* orow_g =
-        reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D + hl * kOHalf;
-#pragma unroll
-    for (int c = 0; c < kOHalf / 32; ++c) {
-      uint32_t orow[32];
-      if (my_n_kv > 0) {
-        tmem_ld_16x32bx2_x32<kOHalf>(tO + c * 32, orow);
-        tmem_wait_ld();
-        reg_fence(orow);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) orow[i] = 0u;
-      }
-      uint32_t packed[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
-                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
-      if (grow < S) {
-        uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
-                              packed[4 * i + 3]);
-      }
-    }
-    if (args.lse != nullptr && grow < S && hl == 0)
-      args.lse[size_t(bh) * S + grow] =
-          l_row > 0.f ? (m_run + __log2f(l_row)) * kLn2 : -INFINITY;
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == kRSWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
-}
-
-// ----------------------------------------------------------------------------
 // Descriptor self-test: one 128x128x128 UMMA product, checked on the host.
 //   mode 0: D = A * B^T, A [128][128] K-major, B [128 n][128 k] K-major (QK^T)
 //   mode 1: D = A * B,   A K-major, B [128 k][128 n] MN-major       (PV, SS)
@@ -1038,30 +669,7 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 template <int D, bool kBF16>
-cudaError_t launch_rs(const FwdLaunch& L) {
-  using C = Cfg<D>;
-  auto kern = L.args.trace != nullptr ? sdpa_fwd_rs_kernel<D, kBF16, true>
-                                      : sdpa_fwd_rs_kernel<D, kBF16, false>;
-  static bool attr_set[64][2] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int tr = L.args.trace != nullptr;
-  if (dev < 64 && !attr_set[dev][tr]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set[dev][tr] = true;
-  }
-  const int rows_per_cta = kBM * kQTiles;
-  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
-  kern<<<grid, kThreadsRS, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
-      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
-  return cudaGetLastError();
-}
-
-template <int D, bool kBF16>
 cudaError_t launch_typed(const FwdLaunch& L) {
-  if (L.variant == 2) return launch_rs<D, kBF16>(L);
   using C = Cfg<D>;
   auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true>
                                       : sdpa_fwd_kernel<D, kBF16, false>;
@@ -1084,17 +692,17 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 
 }  // namespace
 
-FwdGeometry fwd_geometry(int64_t S, int64_t BH, int variant) {
+FwdGeometry fwd_geometry(int64_t S, int64_t BH) {
   FwdGeometry g;
   g.block_m = kBM;
   g.block_n = kBN;
   g.q_tiles_per_cta = kQTiles;
-  g.threads = variant == 2 ? kThreadsRS : kThreads;
+  g.threads = kThreads;
   g.ctas = ((S + kBM * g.q_tiles_per_cta - 1) / (kBM * g.q_tiles_per_cta)) * BH;
   return g;
 }
 
-int fwd_ring_slots(int D, int variant) {
+int fwd_ring_slots(int D) {
   return D == 128 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
 }
 

@@ -63,7 +63,6 @@ struct FwdLaunch {
   int64_t bh;
   int head_dim;
   bool bf16;
-  int variant;  // 0 = two Q tiles ping-pong, 1 = one Q tile, double-buffered S
   void* stream;
 };
 
@@ -75,8 +74,8 @@ struct FwdGeometry {
   int64_t ctas;
 };
 
-FwdGeometry fwd_geometry(int64_t S, int64_t BH, int variant);
-int fwd_ring_slots(int D, int variant);
+FwdGeometry fwd_geometry(int64_t S, int64_t BH);
+int fwd_ring_slots(int D);
 cudaError_t launch_sdpa_fwd(const FwdLaunch& launch);
 cudaError_t launch_umma_selftest(const CUtensorMap* a_map, const CUtensorMap* b_map,
                                  const void* a_glob, float* d_out, int mode, bool bf16,

@@ -1,5 +1,5 @@
-"""A/B timing of library builds x kernel variants on one config (tuning aid).
-usage: python scripts/ab_libs.py B H S D lib1[:v1,v2] lib2[:v...] ..."""
+"""A/B timing of library builds (e.g. -D tuning macros, see _build.py) on one
+config (tuning aid).  usage: python scripts/ab_libs.py B H S D lib1 lib2 ..."""
 import os, subprocess, sys
 B, H, S, D = sys.argv[1:5]
 code = r'''
@@ -22,8 +22,7 @@ err = (o[:, :2].float() - ref.float()).abs().max().item()
 print(f"{ms:.3f} ms {4*B*H*S*S*D/ms/1e9:7.1f} TF/s err {err:.1e}")
 '''
 for spec in sys.argv[5:]:
-    lib, _, vs = spec.partition(":")
-    for v in (vs.split(",") if vs else ["0"]):
-        env = dict(os.environ, TILEATTN_B200_LIB=os.path.abspath(lib), TILEATTN_B200_VARIANT=v)
-        r = subprocess.run([sys.executable, "-c", code, B, H, S, D], env=env, capture_output=True, text=True)
-        print(f"{os.path.basename(lib):24s} v{v}: {(r.stdout.strip() or r.stderr.strip()[-300:])}", flush=True)
+    lib = spec
+    env = dict(os.environ, TILEATTN_B200_LIB=os.path.abspath(lib))
+    r = subprocess.run([sys.executable, "-c", code, B, H, S, D], env=env, capture_output=True, text=True)
+    print(f"{os.path.basename(lib):24s}: {(r.stdout.strip() or r.stderr.strip()[-300:])}", flush=True)
