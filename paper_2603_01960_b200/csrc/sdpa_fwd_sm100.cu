@@ -94,12 +94,19 @@ constexpr float kSumGuard = 256.0f;
 #define TA_MMA_BATCH 1
 #endif
 
+#ifndef TA_SLOTS_D128
+#define TA_SLOTS_D128 4
+#endif
+#ifndef TA_KV_EVICT_LAST
+#define TA_KV_EVICT_LAST 0
+#endif
+
 template <int D>
 struct Cfg {
   static constexpr int kRegions = D / 64;                   // 128-B swizzle atoms along D
   static constexpr int kTileBytes = kBM * D * 2;            // one Q / K / V tile
   static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
-  static constexpr int kSlots = D == 128 ? 4 : 8;           // K/V ring depth
+  static constexpr int kSlots = D == 128 ? TA_SLOTS_D128 : 8;  // K/V ring depth
   static constexpr int kSmemData = kQTiles * kTileBytes + kSlots * kTileBytes;
   static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/;
   static constexpr uint32_t kTmemS = 0;      // S0 at col 0, S1 at col 128 (fp32)
@@ -194,6 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int r = 0; r < C::kRegions; ++r)
           tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
                       q0 + t * kBM, bh);
+#if TA_KV_EVICT_LAST
+      const uint64_t kv_policy = l2_policy_evict_last();  // K/V re-read by the head's CTAs
+#endif
       int slot = 0;
       uint32_t phase = 0;
       for (int j = 0; j < n_kv; ++j) {
@@ -203,8 +213,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(fbar, C::kTileBytes);
           const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
           for (int r = 0; r < C::kRegions; ++r)
+#if TA_KV_EVICT_LAST
+            tma_load_3d_hint(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
+                             j * kBN, bh, kv_policy);
+#else
             tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
                         j * kBN, bh);
+#endif
           if (++slot == C::kSlots) {
             slot = 0;
             phase ^= 1;
