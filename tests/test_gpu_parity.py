@@ -132,6 +132,28 @@ def test_large_scores_exercise_lazy_rescale(ta, cuda_device):
     assert np.abs(lse - r["lse"]).max() <= LSE_TOL * 10  # |LSE| ~ 40 here
 
 
+@pytest.mark.parametrize("dt", [O.BF16, O.F16])
+def test_running_max_jumps_in_later_halves(ta, cuda_device, dt):
+    # Scores stay small except planted keys aligned with q, each exceeding
+    # the running max by > 2^8 (log2 units) in the first or second half of a
+    # later K/V tile: drives every branch of the lazy rescale (the D=128
+    # stale-max slow path for half 0 and half 1, and the exact-max path at
+    # D=64) against the oracle.
+    for D in (64, 128):
+        q, k, v = O.make_input((1, 4, 512, D), dt, 91)
+        q = np.full_like(q, 0.5)          # every row = 0.5 * ones (on the 16-bit grid)
+        k = k * np.float32(0.125)         # exact power-of-2 scaling keeps k on the grid
+        spikes = {0: [256 + 10], 1: [256 + 64 + 10], 2: [128 + 70, 384 + 100],
+                  3: [64 + 3, 192 + 5, 256 + 66, 448 + 50]}
+        for h, keys in spikes.items():
+            for n, key in enumerate(keys):
+                k[0, h, key, :] = np.float32(1.5 + n)  # score grows at each planted key
+        o, lse = run_gpu(ta, q, k, v, dt)
+        r = oracle_ref(q, k, v)
+        assert np.abs(o - r["o"]).max() <= TOL[dt], D
+        assert np.abs(lse - r["lse"]).max() <= LSE_TOL * 4, D
+
+
 # ------------------------------------------------- larger S, sampled heads
 @pytest.mark.parametrize("D,dt", [(64, O.BF16), (128, O.BF16), (128, O.F16)])
 def test_long_sequence_sampled_heads(ta, cuda_device, D, dt):
