@@ -8,8 +8,9 @@
 // borrowed f32-on-the-16-bit-grid tensor, the output is returned by value and
 // snapped to the dtype grid (tiled.cpp:216-220); std::invalid_argument for bad
 // shapes / masks / scales, UnsupportedScheduleError for bad schedules and for
-// what the sm_100a kernel does not cover (F32 / F64 accumulation, D not in
-// {64,128}).  Header-only: include it and link libtileattn_b200.so.
+// what the sm_100a kernel does not cover (F32 / F64 accumulation, D not a
+// multiple of 8 or above 128).  Header-only: include it and link
+// libtileattn_b200.so.
 #pragma once
 
 #include <atomic>

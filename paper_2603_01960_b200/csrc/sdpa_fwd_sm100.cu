@@ -559,7 +559,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int grow = q0 + t * kBM + row;
     const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * D;
+    const int dm = args.head_dim;  // stored columns (<= D)
+    uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * dm;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t orow[32];
@@ -579,9 +580,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (grow < S) {
         uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
-                              packed[4 * i + 3]);
+        for (int i = 0; i < 4; ++i)  // 16-B pieces of 8 columns; dm is a multiple of 8
+          if (c * 32 + i * 8 < dm)
+            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                                packed[4 * i + 3]);
       }
     }
     if (args.lse != nullptr && grow < S)

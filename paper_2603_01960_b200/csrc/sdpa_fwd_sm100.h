@@ -18,6 +18,8 @@ struct FwdArgs {
   void* o;           // [BH, S, D] 16-bit, same dtype as inputs
   float* lse;        // [BH, S] fp32 natural-log LSE, or nullptr
   int seq_len;       // S
+  int head_dim;      // D of the tensors in memory (<= the kernel's D; the
+                     // kernel's extra columns are TMA zero-fill)
   float scale_log2;  // softmax scale * log2(e)
   int mask;          // FwdMask
   int heads;         // H: batch index of flattened head bh is (bh_offset + bh) / H
@@ -61,7 +63,7 @@ struct FwdLaunch {
   const CUtensorMap* tmap_v;
   FwdArgs args;
   int64_t bh;
-  int head_dim;
+  int head_dim;  // kernel instantiation: 64 or 128
   bool bf16;
   void* stream;
 };

@@ -125,9 +125,11 @@ static void test_validation_order_and_classes() {  // tiled.cpp:256-259, types.c
   const AttnInput f32 = make_input(Shape{1, 1, 32, 64}, DType::F32, 1);
   CHECK_THROWS_AS(sdpa_tiled(f32, MaskSpec::none(), ScaleSpec{}, TileSchedule{}, cache),
                   UnsupportedScheduleError);
-  const AttnInput d48 = make_input(Shape{1, 2, 32, 48}, DType::BF16Emu, 77);
-  CHECK_THROWS_AS(sdpa_tiled(d48, MaskSpec::none(), ScaleSpec{}, TileSchedule{}, cache),
-                  UnsupportedScheduleError);
+  for (int64_t d : {44, 160}) {  // not a multiple of 8 / above 128
+    const AttnInput odd = make_input(Shape{1, 2, 32, d}, DType::BF16Emu, 77);
+    CHECK_THROWS_AS(sdpa_tiled(odd, MaskSpec::none(), ScaleSpec{}, TileSchedule{}, cache),
+                    UnsupportedScheduleError);
+  }
   TiledOptions f64;
   f64.accum = AccumMode::F64;
   CHECK_THROWS_AS(sdpa_tiled(in, MaskSpec::none(), ScaleSpec{}, TileSchedule{}, cache, f64),
@@ -139,7 +141,7 @@ static void test_tiled_kernel_matches_the_reference_oracle() {  // test_tiled.cp
   PlanCache cache;
   for (int64_t s : {32, 130}) {
     for (DType dt : {DType::F16Emu, DType::BF16Emu}) {
-      for (int64_t d : {64, 128}) {
+      for (int64_t d : {64, 96, 128}) {
         const AttnInput in = make_input(Shape{1, 2, s, d}, dt, 77);
         for (const MaskSpec& mask : {MaskSpec::none(), MaskSpec::causal(),
                                      MaskSpec::padding({std::max<int64_t>(1, s / 2)})}) {

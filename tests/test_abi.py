@@ -90,7 +90,9 @@ def test_validation_order_and_error_classes():
     with pytest.raises(ta.UnsupportedScheduleError):
         _call(dtype=ta.F32)
     with pytest.raises(ta.UnsupportedScheduleError):
-        _call(shape=(1, 1, 64, 48))
+        _call(shape=(1, 1, 64, 44))
+    with pytest.raises(ta.UnsupportedScheduleError):
+        _call(shape=(1, 1, 64, 160))
 
 
 def test_no_cpu_fallback_without_device():

@@ -154,6 +154,21 @@ def test_running_max_jumps_in_later_halves(ta, cuda_device, dt):
         assert np.abs(lse - r["lse"]).max() <= LSE_TOL * 4, D
 
 
+# ------------------------------------------- head dims other than 64 / 128
+@pytest.mark.parametrize("dt", [O.BF16, O.F16])
+@pytest.mark.parametrize("D", [8, 32, 48, 80, 96, 120])
+def test_other_head_dims_match_oracle(ta, cuda_device, dt, D):
+    # D <= 64 runs the D=64 kernel, D <= 128 the D=128 kernel, the columns
+    # past D zero-filled by TMA (the paper's grid has D=96)
+    q, k, v = O.make_input((2, 2, 300, D), dt, 1000 + D)
+    for causal in (False, True):
+        o, lse = run_gpu(ta, q, k, v, dt, causal=causal)
+        r = oracle_ref(q, k, v, mask_kind=O.MASK_CAUSAL if causal else O.MASK_NONE)
+        assert o.shape == q.shape
+        assert np.abs(o - r["o"]).max() <= TOL[dt], (D, causal)
+        assert np.abs(lse - r["lse"]).max() <= LSE_TOL, (D, causal)
+
+
 # ------------------------------------------------- larger S, sampled heads
 @pytest.mark.parametrize("D,dt", [(64, O.BF16), (128, O.BF16), (128, O.F16)])
 def test_long_sequence_sampled_heads(ta, cuda_device, D, dt):
@@ -226,9 +241,10 @@ def test_stats_report_executed_tiling(ta, cuda_device):
 
 def test_errors_are_loud(ta, cuda_device):
     import torch
-    x = torch.zeros(1, 1, 64, 48, device="cuda", dtype=torch.bfloat16)
-    with pytest.raises(ta.UnsupportedScheduleError):
-        ta.sdpa(x, x, x)
+    for d in (44, 160):  # not a multiple of 8 / above the TMEM budget
+        x = torch.zeros(1, 1, 64, d, device="cuda", dtype=torch.bfloat16)
+        with pytest.raises(ta.UnsupportedScheduleError):
+            ta.sdpa(x, x, x)
     y = torch.zeros(1, 1, 64, 64, device="cuda", dtype=torch.float32)
     with pytest.raises(ta.UnsupportedScheduleError):
         ta.sdpa(y, y, y)
