@@ -1,0 +1,79 @@
+"""Harness integration: the reference's own benchmark
+harness (bench.cpp / analysis.cpp, compiled unmodified into
+oracle/_ref/b200_grid by oracle/Makefile) with the B200 operator registered
+as method "b200" by integration/b200_method.cpp.  The grid writes the
+reference's 17-column CSV and JSON manifest (bench.hpp:156-176); each b200
+point passes the reference's correctness gate (check_correctness against
+sdpa_reference, bench.cpp:270-290) before it is timed."""
+import csv
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GRID = ROOT / "oracle" / "_ref" / "b200_grid"
+HEADER = ("method,B,H,S,D,dtype,causal,t_m,t_n,stages,layout,median_ms,p95_ms,"
+          "tokens_per_s,bw_proxy,status,status_detail").split(",")
+
+needs_grid = pytest.mark.skipif(not GRID.exists(), reason="oracle/_ref/b200_grid not built")
+
+
+def run_grid(tmp_path, *args):
+    out = tmp_path / "grid"
+    r = subprocess.run([str(GRID), *args, "--out", str(out)], capture_output=True, text=True,
+                       timeout=600)
+    return r, out
+
+
+def read(out):
+    with open(out / "results.csv") as f:
+        rows = list(csv.reader(f))
+    assert rows[0] == HEADER
+    assert all(len(r) == 17 for r in rows)
+    return [dict(zip(HEADER, r)) for r in rows[1:]]
+
+
+@needs_grid
+def test_reference_methods_through_the_harness(tmp_path):
+    r, out = run_grid(tmp_path, "--methods", "tiled", "--s", "64,300", "--d", "64",
+                      "--dtypes", "bf16", "--masks", "none,causal", "--b", "1", "--h", "2",
+                      "--warmup", "1", "--timed", "3")
+    assert r.returncode == 0, r.stderr
+    rows = read(out)
+    assert len(rows) == 4 and all(x["status"] == "ok" for x in rows)
+    m = json.loads((out / "manifest.json").read_text())
+    assert m["n_timed"] == 3 and "tileattn_b200" in m["artifact_version"]
+
+
+@needs_grid
+def test_b200_method_fails_loudly_without_a_device(tmp_path):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("host has a GPU")
+    r, _ = run_grid(tmp_path, "--methods", "b200", "--s", "64", "--d", "64", "--dtypes", "bf16",
+                    "--masks", "none", "--warmup", "1", "--timed", "3")
+    assert r.returncode != 0 and "CUDA" in r.stderr
+
+
+@pytest.mark.gpu
+@needs_grid
+def test_b200_method_in_the_reference_grid(tmp_path, cuda_device):
+    r, out = run_grid(tmp_path, "--methods", "b200,tiled", "--s", "128,512", "--d", "64,96,160",
+                      "--dtypes", "f16,bf16", "--masks", "none,causal", "--b", "1", "--h", "2",
+                      "--warmup", "1", "--timed", "3")
+    assert r.returncode == 0, r.stderr
+    rows = read(out)
+    assert len(rows) == 2 * 2 * 3 * 2 * 2
+    ours = [x for x in rows if x["method"] == "b200"]
+    ref = {(x["S"], x["D"], x["dtype"], x["causal"]): x for x in rows if x["method"] == "tiled"}
+    for x in ours:
+        if x["D"] == "160":  # beyond the kernel's TMEM budget: the harness's unsupported row
+            assert x["status"] == "unsupported" and x["median_ms"] == "NaN"
+            continue
+        assert x["status"] == "ok", x  # passed the reference's correctness gate
+        assert (x["t_m"], x["t_n"], x["stages"], x["layout"]) == ("64", "128", "2", "row")
+        if x["S"] == "512":
+            cpu = ref[(x["S"], x["D"], x["dtype"], x["causal"])]
+            assert float(x["median_ms"]) < float(cpu["median_ms"])
