@@ -289,7 +289,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
 // per-device workspace for the host-buffer entry: device buffers plus the
 // copy streams / events of the chunked H2D -> compute -> D2H pipeline
 struct Workspace {
-  static constexpr int kMaxChunks = 16;
+  static constexpr int kMaxChunks = 64;
   std::mutex mu;
   void* ptr = nullptr;
   size_t bytes = 0;
@@ -433,7 +433,13 @@ ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o,
   // stream (heads are independent and contiguous in [B*H, S, D]).
   const int64_t bh = shape.b * shape.h;
   const size_t head_elems = size_t(shape.s * shape.d);
-  const int n_chunks = int(n * 2 >= (size_t(64) << 20) ? std::min<int64_t>(bh, 16) : 1);
+  // ~64 MiB+ tensors: up to 64 chunks (the pipeline fill and drain are one
+  // chunk's H2D and one chunk's compute + D2H; the H2D stream itself runs at
+  // the PCIe rate the whole time), never below 8 MiB per input chunk
+  const int64_t max_chunks = std::max<int64_t>(1, int64_t(n * 2 / (size_t(8) << 20)));
+  const int n_chunks = int(n * 2 >= (size_t(64) << 20)
+                               ? std::min<int64_t>({bh, int64_t(Workspace::kMaxChunks), max_chunks})
+                               : 1);
   if ((st = ws.ensure_streams()) != TA_OK) return st;
   int64_t h0 = 0;
   for (int c = 0; c < n_chunks; ++c) {
