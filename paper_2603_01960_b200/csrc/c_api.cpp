@@ -95,7 +95,8 @@ ta_status validate_device_support(ta_shape sh, ta_dtype dt, ta_mask_kind mask) {
     return fail(TA_ERR_UNSUPPORTED, "padding masks support B <= " +
                                         std::to_string(ta::kMaxPaddingBatch));
   if (sh.s > (int64_t(1) << 30)) return fail(TA_ERR_UNSUPPORTED, "S too large");
-  if (sh.b * sh.h > 65535) return fail(TA_ERR_UNSUPPORTED, "B*H > 65535");
+  if (((sh.s + 255) / 256) * sh.b * sh.h > 0x7FFFFFFF)
+    return fail(TA_ERR_UNSUPPORTED, "more than 2^31 - 1 work items (B*H*ceil(S/256))");
   return TA_OK;
 }
 

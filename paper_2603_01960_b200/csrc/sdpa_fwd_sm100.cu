@@ -144,9 +144,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int S = args.seq_len;
-  const int bh = blockIdx.y;
+  // 1-D grid over (head, query block), query block fastest (concurrent CTAs
+  // share a head's K/V in L2); no 65535 limit on B*H
+  const int n_qblk = (args.seq_len + kBM * kQTiles - 1) / (kBM * kQTiles);
+  const int bh = int(blockIdx.x) / n_qblk;
+  const int qblk_in = int(blockIdx.x) - bh * n_qblk;
   // causal: heaviest query blocks first (longest-processing-time order)
-  const int qblk = args.mask == kMaskCausal ? int(gridDim.x - 1 - blockIdx.x) : int(blockIdx.x);
+  const int qblk = args.mask == kMaskCausal ? n_qblk - 1 - qblk_in : qblk_in;
   const int q0 = qblk * (kBM * kQTiles);
   // keys admitted by the mask (reference MaskSpec::admits, types.hpp:48-67):
   // None -> j < S; Padding -> j < valid_len[b]; Causal -> j <= i, which also
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int t = 0; t < kQTiles; ++t)
     n_kv_t[t] = args.mask == kMaskCausal ? min(diag0 + t + 1, n_kv_seq) : n_kv_seq;
   const int n_kv = n_kv_t[kQTiles - 1];  // K/V tiles streamed (max over the Q tiles)
-  long long* const trace = (kTrace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+  long long* const trace = (kTrace && blockIdx.x == 0) ? args.trace : nullptr;
   auto rec = [&](int ev, int j) {
     if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
   };
@@ -701,7 +705,9 @@ cudaError_t launch_typed(const FwdLaunch& L) {
     attr_set[dev][tr] = true;
   }
   const int rows_per_cta = kBM * kQTiles;
-  dim3 grid((L.args.seq_len + rows_per_cta - 1) / rows_per_cta, L.bh);
+  const int64_t ctas = int64_t((L.args.seq_len + rows_per_cta - 1) / rows_per_cta) * L.bh;
+  if (ctas > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
+  const dim3 grid(static_cast<unsigned int>(ctas), 1u, 1u);
   kern<<<grid, kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
       *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
   return cudaGetLastError();

@@ -54,6 +54,8 @@ enum TraceEvent {
   kEvSm0ArriveW1,  // Q tile 0, warps 1..3: last P part arrived (warp skew)
   kEvSm0ArriveW2,
   kEvSm0ArriveW3,
+  kEvKernelStart,  // [0]: CTA entry; [1]: after the TMEM alloc / barrier-init sync
+  kEvEpilogueDone,  // [t]: Q tile t's row-0 warp has stored O and LSE
   kNumTraceEvents
 };
 

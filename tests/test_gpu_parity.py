@@ -169,6 +169,20 @@ def test_other_head_dims_match_oracle(ta, cuda_device, dt, D):
         assert np.abs(lse - r["lse"]).max() <= LSE_TOL, (D, causal)
 
 
+def test_many_heads_beyond_the_old_grid_y_limit(ta, cuda_device):
+    # B*H = 70,000 > 65,535 (a 2-D grid's y limit): the 1-D grid covers it
+    import torch
+    B, H, S, D = 7000, 10, 16, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=torch.bfloat16, generator=g)
+               for _ in range(3))
+    o = ta.sdpa(q, k, v)
+    torch.cuda.synchronize()
+    for b, h in ((0, 0), (3456, 7), (6999, 9)):
+        ref = torch.softmax((q[b, h].float() @ k[b, h].float().T) / 8.0, dim=-1) @ v[b, h].float()
+        assert (o[b, h].float() - ref).abs().max().item() <= TOL[O.BF16]
+
+
 # ------------------------------------------------- larger S, sampled heads
 @pytest.mark.parametrize("D,dt", [(64, O.BF16), (128, O.BF16), (128, O.F16)])
 def test_long_sequence_sampled_heads(ta, cuda_device, D, dt):
