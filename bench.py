@@ -345,18 +345,24 @@ def run_sweep(args):
         ("ViT B64 H16 S1024 D64 bf16", 64, 16, 1024, 64, torch.bfloat16),
         ("long B8 H64 S32768 D128 bf16", 8, 64, 32768, 128, torch.bfloat16),
     ]
+    # causal twins (half the paper's grid): same FLOP convention
+    # as the reference's flop_rate (4*B*H*S^2*D); "causal_effective_tflops"
+    # counts the admitted half only
+    causal = [("D-sweep B8 H32 S4096 D128 bf16 causal", 8, 32, 4096, 128, torch.bfloat16),
+              ("long B8 H64 S32768 D128 bf16 causal", 8, 64, 32768, 128, torch.bfloat16)]
     rows = []
-    for name, B, H, S, D, dt in configs:
+    for name, B, H, S, D, dt in configs + causal:
+        is_causal = name.endswith("causal")
         q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=dt) for _ in range(3))
         o = torch.empty_like(q)
         for _ in range(3):
-            ta.sdpa(q, k, v, out=o)
+            ta.sdpa(q, k, v, out=o, causal=is_causal)
         torch.cuda.synchronize()
         n = 3 if S >= 32768 else 20
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(n):
-            ta.sdpa(q, k, v, out=o)
+            ta.sdpa(q, k, v, out=o, causal=is_causal)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / n
@@ -364,14 +370,15 @@ def run_sweep(args):
         ref_ms = None
         if args.vendor:
             for _ in range(2):
-                torch.nn.functional.scaled_dot_product_attention(q, k, v)
+                torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=is_causal)
             e0.record()
             for _ in range(n):
-                torch.nn.functional.scaled_dot_product_attention(q, k, v)
+                torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=is_causal)
             e1.record()
             torch.cuda.synchronize()
             ref_ms = e0.elapsed_time(e1) / n
         rows.append(dict(config=name, ms=ms, tflops=tf, frac=tf / pk["bf16_tflops"],
+                         causal_effective_tflops=tf / 2 if is_causal else None,
                          hbm_gbs=(8 * B * H * S * D + 4 * B * H * S) / ms / 1e6,
                          torch_sdpa_ms=ref_ms,
                          torch_sdpa_tflops=(flops(B, H, S, D) / ref_ms / 1e9) if ref_ms else None))
