@@ -130,7 +130,7 @@ std::shared_ptr<const Plan> get_plan(const ta_schedule& s, int64_t d, ta_dtype d
       return it->second;
     }
   }
-  auto g = ta::fwd_geometry(1, 1);
+  auto g = ta::fwd_geometry(1, 1, d);
   auto plan = std::make_shared<const Plan>(
       Plan{g.block_m, g.block_n, ta::fwd_ring_slots(int(d)), g.q_tiles_per_cta, g.threads});
   c.constructions.fetch_add(1, std::memory_order_relaxed);
@@ -218,7 +218,7 @@ void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh, ta_mask_kind ma
   const int64_t bh = sh.b * sh.h;
   const int64_t q_tiles = (sh.s + p.block_m - 1) / p.block_m;
   const int64_t kv_tiles = (sh.s + p.block_n - 1) / p.block_n;
-  const auto g = ta::fwd_geometry(sh.s, bh);
+  const auto g = ta::fwd_geometry(sh.s, bh, sh.d);
   uint64_t visited = 0;
   if (mask == TA_MASK_CAUSAL) {
     for (int64_t qt = 0; qt < q_tiles; ++qt) {

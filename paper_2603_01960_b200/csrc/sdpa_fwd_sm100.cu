@@ -27,41 +27,53 @@
 #include "ptx_sm100.cuh"
 #include "sdpa_fwd_sm100.h"
 
+// Roles<kQT> constants are used through local aliases; the front end reports
+// the static members as unreferenced (#177) for some instantiations.
+#pragma nv_diag_suppress 177
+
 namespace ta {
 namespace {
 
 constexpr int kBM = 128;        // rows per Q tile (UMMA M)
 constexpr int kBN = 128;        // keys per K/V tile (UMMA N of QK^T, K of PV)
-constexpr int kQTiles = 2;      // Q tiles per CTA (ping-pong)
-constexpr int kThreads = 384;   // 12 warps
-// Warp roles.  The SM's warp arbiter favours the highest warp id among
-// eligible warps, so the latency-critical single-thread roles (MMA issue, TMA)
-// take the top ids and are never starved by the softmax warps' issue stream.
-constexpr int kNumSoftmaxWarps = 8;  // softmax warps s = 0..3 -> Q tile 0, 4..7 -> Q tile 1
-// Control warps either below (TA_CONTROL_LOW) or above the softmax warps.
-// The warp scheduler prefers higher warp ids: control-high gives the MMA
-// warp priority on its SMSP (fast issue), control-low gives the softmax
-// warp sharing that SMSP priority (less skew between the 4 softmax warps).
-#ifndef TA_CONTROL_LOW
-#define TA_CONTROL_LOW 0
+constexpr int kQTiles = 2;      // max Q tiles per CTA (ping-pong)
+
+// Warp roles and register split of a CTA with kQT Q tiles (kQT = 2: the
+// D=128 ping-pong, one CTA per SM; kQT = 1: D=64, two CTAs per SM, each
+// with one Q tile, so one CTA's prologue / epilogue overlaps the other's
+// loop).  Softmax warps 4t..4t+3 own Q tile t (warp w <-> TMEM lane quadrant
+// w % 4); the control warps take the top ids (the SM's warp arbiter favours
+// high ids, so the single-thread roles are never starved).
+template <int kQT>
+struct Roles {
+  static constexpr int kSoftmaxWarps = 4 * kQT;
+  static constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
+  static constexpr int kMinBlocks = kQT == 1 ? 2 : 1;
+  static constexpr int kWarpAlloc = kSoftmaxWarps + 0;  // TMEM allocator (otherwise idle)
+  static constexpr int kWarpTma = kSoftmaxWarps + 1;
+  static constexpr int kWarpTrace = kSoftmaxWarps + 2;  // diagnostics only
+  static constexpr int kWarpMma = kSoftmaxWarps + 3;
+  static constexpr uint32_t kTmemCols = kQT == 1 ? 256 : 512;
+  // setmaxnreg.inc only draws on registers released by setmaxnreg.dec in
+  // the same CTA, so the split must balance around the launch allocation
+  // (kQT=2: 65536/384 -> 168, 256*(208-168) == 128*(168-88); kQT=1, two
+  // CTAs: 32768/256 -> 128, 128*(208-128) == 128*(128-48)).
+  static constexpr int kLaunchRegs = (65536 / (kThreads * kMinBlocks)) & ~7;
+  static constexpr int kRegsSoftmax = 208;
+  static constexpr int kRegsControl = kQT == 1 ? 48 : 88;
+  static_assert(kSoftmaxWarps * 32 * (kRegsSoftmax - kLaunchRegs) <=
+                    (kThreads - kSoftmaxWarps * 32) * (kLaunchRegs - kRegsControl),
+                "setmaxnreg.inc would wait forever: register pool does not balance");
+};
+// Q tiles per CTA by head dim (TA_D64_TILES: 1 or 2 for A/B builds)
+#ifndef TA_D64_TILES
+#define TA_D64_TILES 1
 #endif
-constexpr int kSoftmaxBase = TA_CONTROL_LOW ? 4 : 0;  // first softmax warp
-constexpr int kCtl = TA_CONTROL_LOW ? 0 : 8;          // first control warp
-constexpr int kWarpAlloc = kCtl + 0;  // TMEM allocator (otherwise idle)
-constexpr int kWarpTma = kCtl + 1;
-constexpr int kWarpTrace = kCtl + 2;  // diagnostics only
-constexpr int kWarpMma = kCtl + 3;
-constexpr uint32_t kTmemCols = 512;
-// register split: 4 control warps (TMA, MMA, TMEM alloc, spare) + 8 softmax warps
-// setmaxnreg.inc only draws on registers released by setmaxnreg.dec in the
-// same CTA, so the split must balance around the launch allocation
-// (65536 / 384 threads -> 168 per thread): 256*(208-168) == 128*(168-88).
-constexpr int kLaunchRegs = (65536 / kThreads) & ~7;
-constexpr int kRegsControl = 88;
-constexpr int kRegsSoftmax = 208;
-static_assert(kNumSoftmaxWarps * 32 * (kRegsSoftmax - kLaunchRegs) <=
-                  (kThreads - kNumSoftmaxWarps * 32) * (kLaunchRegs - kRegsControl),
-              "setmaxnreg.inc would wait forever: register pool does not balance");
+#ifndef TA_D128_TILES
+#define TA_D128_TILES 2
+#endif
+template <int D>
+constexpr int kQTilesFor = D == 64 ? TA_D64_TILES : TA_D128_TILES;
 constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
@@ -97,20 +109,18 @@ constexpr float kSumGuard = 256.0f;
 #ifndef TA_SLOTS_D128
 #define TA_SLOTS_D128 4
 #endif
-#ifndef TA_KV_EVICT_LAST
-#define TA_KV_EVICT_LAST 0
-#endif
 
-template <int D>
+template <int D, int kQT = kQTilesFor<D>>
 struct Cfg {
   static constexpr int kRegions = D / 64;                   // 128-B swizzle atoms along D
   static constexpr int kTileBytes = kBM * D * 2;            // one Q / K / V tile
   static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
-  static constexpr int kSlots = D == 128 ? TA_SLOTS_D128 : 8;  // K/V ring depth
-  static constexpr int kSmemData = kQTiles * kTileBytes + kSlots * kTileBytes;
+  // K/V ring depth (two CTAs per SM at kQT = 1: 16 KB Q + 4 x 16 KB ring each)
+  static constexpr int kSlots = D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128) : kQT == 1 ? 4 : 8;
+  static constexpr int kSmemData = kQT * kTileBytes + kSlots * kTileBytes;
   static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/;
-  static constexpr uint32_t kTmemS = 0;      // S0 at col 0, S1 at col 128 (fp32)
-  static constexpr uint32_t kTmemO = 256;    // O0 at 256, O1 at 256 + D (fp32)
+  static constexpr uint32_t kTmemS = 0;                  // S_t at col 128 t (fp32)
+  static constexpr uint32_t kTmemO = 128 * kQT;          // O_t at kTmemO + D t (fp32)
 };
 
 struct Barriers {
@@ -124,12 +134,15 @@ struct Barriers {
   uint32_t tmem_base;
 };
 
-template <int D, bool kBF16, bool kTrace>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>>
+__global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
     sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
-  using C = Cfg<D>;
+  using C = Cfg<D, kQT>;
+  using R = Roles<kQT>;
+  constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
+                kWarpMma = R::kWarpMma;
   // the stale-max softmax pays off where the softmax is on the critical path
   // of a tensor-bound loop (D=128); at D=64 the kernel is softmax-throughput
   // bound and the extra o_half commit costs more than the saved row max
@@ -138,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const uint32_t sq = smem_u32(smem);                          // Q tiles
-  const uint32_t sring = sq + kQTiles * C::kTileBytes;         // K/V ring
+  const uint32_t sring = sq + kQT * C::kTileBytes;             // K/V ring
   Barriers* bars = reinterpret_cast<Barriers*>(smem + C::kSmemData);
 
   const uint32_t warp = warp_id();
@@ -146,12 +159,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = args.seq_len;
   // 1-D grid over (head, query block), query block fastest (concurrent CTAs
   // share a head's K/V in L2); no 65535 limit on B*H
-  const int n_qblk = (args.seq_len + kBM * kQTiles - 1) / (kBM * kQTiles);
+  const int n_qblk = (args.seq_len + kBM * kQT - 1) / (kBM * kQT);
   const int bh = int(blockIdx.x) / n_qblk;
   const int qblk_in = int(blockIdx.x) - bh * n_qblk;
   // causal: heaviest query blocks first (longest-processing-time order)
   const int qblk = args.mask == kMaskCausal ? n_qblk - 1 - qblk_in : qblk_in;
-  const int q0 = qblk * (kBM * kQTiles);
+  const int q0 = qblk * (kBM * kQT);
   // keys admitted by the mask (reference MaskSpec::admits, types.hpp:48-67):
   // None -> j < S; Padding -> j < valid_len[b]; Causal -> j <= i, which also
   // bounds the K/V tiles a query tile visits (kv_end = last_row / t_n + 1,
@@ -160,11 +173,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
   const int n_kv_seq = (kv_len + kBN - 1) / kBN;
   const int diag0 = q0 / kBN;  // K/V tile on Q tile 0's diagonal
-  int n_kv_t[kQTiles];
+  int n_kv_t[kQTiles] = {0, 0};
 #pragma unroll
-  for (int t = 0; t < kQTiles; ++t)
+  for (int t = 0; t < kQT; ++t)
     n_kv_t[t] = args.mask == kMaskCausal ? min(diag0 + t + 1, n_kv_seq) : n_kv_seq;
-  const int n_kv = n_kv_t[kQTiles - 1];  // K/V tiles streamed (max over the Q tiles)
+  const int n_kv = n_kv_t[kQT - 1];  // K/V tiles streamed (max over the Q tiles)
   long long* const trace = (kTrace && blockIdx.x == 0) ? args.trace : nullptr;
   auto rec = [&](int ev, int j) {
     if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
@@ -172,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == kWarpMma * 32) {
     mbar_init(smem_u32(&bars->q_full), 1);
-    for (int t = 0; t < kQTiles; ++t) {
+    for (int t = 0; t < kQT; ++t) {
       mbar_init(smem_u32(&bars->s_full[t]), 1);
       for (int q = 0; q < kPParts; ++q)
         mbar_init(smem_u32(&bars->p_full[t][q]), kBM / 32);  // one arrive per warp
@@ -185,14 +198,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == kWarpAlloc) tmem_alloc<kTmemCols>(smem_u32(&bars->tmem_base));
+  if (warp == kWarpAlloc) tmem_alloc<R::kTmemCols>(smem_u32(&bars->tmem_base));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp - kSoftmaxBase >= uint32_t(kNumSoftmaxWarps)) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
+  if (warp >= uint32_t(R::kSoftmaxWarps)) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::kRegsControl));
   if (warp == kWarpTma) {
     // ------------------------------------------------------------------ TMA
     if (lane == 0) {
@@ -200,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
       const uint32_t qbar = smem_u32(&bars->q_full);
-      if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQTiles * C::kTileBytes);
-      for (int t = 0; t < kQTiles && n_kv > 0; ++t)  // (no key admitted: Q unused)
+      if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQT * C::kTileBytes);
+      for (int t = 0; t < kQT && n_kv > 0; ++t)  // (no key admitted: Q unused)
         for (int r = 0; r < C::kRegions; ++r)
           tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
                       q0 + t * kBM, bh);
@@ -233,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kWarpTrace) {
     // optional tracer: timestamps of tensor-core completions (diagnostics only)
-    if (kTrace && lane == 0 && trace != nullptr) {
+    if (kTrace && kQT == 2 && lane == 0 && trace != nullptr) {
       for (int j = 0; j < n_kv && j < kTraceIters; ++j) {
         mbar_wait(smem_u32(&bars->o_full[0]), uint32_t(j & 1));
         rec(kEvTcPV0Done, j);
@@ -320,9 +333,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
       };
 
+      if constexpr (kQT == 1) {
+        // one Q tile: PV(j-1) once P(j-1) lands, then S(j); the tensor core
+        // idles through this CTA's softmax, which the other CTA on the SM fills
+        const int n = n_kv_t[0];
+        if (n > 0) {
+          mbar_wait(smem_u32(&bars->q_full), 0);
+          tc_fence_after();
+          wait_full(0);
+          issue_qk(0, 0);
+          release(0);
+          for (int j = 1; j < n; ++j) {
+            // S(j) overwrites the S / P columns PV(j-1) reads: in-order
+            // after it on the tensor pipe
+            const int rk = 2 * j, rv = 2 * j - 1;
+            wait_full(rv);
+            issue_pv(0, rv, j > 1, j - 1);
+            release(rv);
+            wait_full(rk);
+            issue_qk(0, rk);
+            release(rk);
+          }
+          const int rv = 2 * n - 1;
+          wait_full(rv);
+          issue_pv(0, rv, n > 1, n - 1);
+          release(rv);
+        }
+      }
       // Q tile 0 visits n0 <= n1 K/V tiles (fewer under the causal mask)
       const int n0 = n_kv_t[0], n1 = n_kv_t[1];
-      if (n1 > 0) {
+      if (kQT == 2 && n1 > 0) {
         mbar_wait(smem_u32(&bars->q_full), 0);
         tc_fence_after();
         wait_full(0);
@@ -350,8 +390,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   } else {
     // -------------------------------------------------------------- softmax
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-    const int t = int(warp - kSoftmaxBase) / 4;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R::kRegsSoftmax));
+    const int t = int(warp) / 4;
     const uint32_t wq = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = int(wq * 32 + lane);
     const uint32_t lane_off = (wq * 32u) << 16;
@@ -598,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == kWarpAlloc) tmem_dealloc<kTmemCols>(tmem);
+  if (warp == kWarpAlloc) tmem_dealloc<R::kTmemCols>(tmem);
 }
 
 // ----------------------------------------------------------------------------
@@ -691,9 +731,10 @@ __global__ void __launch_bounds__(128, 1)
 
 template <int D, bool kBF16>
 cudaError_t launch_typed(const FwdLaunch& L) {
-  using C = Cfg<D>;
-  auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true>
-                                      : sdpa_fwd_kernel<D, kBF16, false>;
+  constexpr int kQT = kQTilesFor<D>;
+  using C = Cfg<D, kQT>;
+  auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true, kQT>
+                                      : sdpa_fwd_kernel<D, kBF16, false, kQT>;
   static bool attr_set[64][2] = {};  // per device, per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
@@ -704,29 +745,30 @@ cudaError_t launch_typed(const FwdLaunch& L) {
     if (e != cudaSuccess) return e;
     attr_set[dev][tr] = true;
   }
-  const int rows_per_cta = kBM * kQTiles;
+  const int rows_per_cta = kBM * kQT;
   const int64_t ctas = int64_t((L.args.seq_len + rows_per_cta - 1) / rows_per_cta) * L.bh;
   if (ctas > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned int>(ctas), 1u, 1u);
-  kern<<<grid, kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+  kern<<<grid, Roles<kQT>::kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
       *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-FwdGeometry fwd_geometry(int64_t S, int64_t BH) {
+FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D) {
+  const int qt = D <= 64 ? kQTilesFor<64> : kQTilesFor<128>;  // NOLINT
   FwdGeometry g;
   g.block_m = kBM;
   g.block_n = kBN;
-  g.q_tiles_per_cta = kQTiles;
-  g.threads = kThreads;
-  g.ctas = ((S + kBM * g.q_tiles_per_cta - 1) / (kBM * g.q_tiles_per_cta)) * BH;
+  g.q_tiles_per_cta = qt;
+  g.threads = qt == 1 ? Roles<1>::kThreads : Roles<2>::kThreads;
+  g.ctas = ((S + kBM * qt - 1) / (kBM * qt)) * BH;
   return g;
 }
 
 int fwd_ring_slots(int D) {
-  return D == 128 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
+  return D > 64 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
 }
 
 cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {

@@ -78,7 +78,7 @@ struct FwdGeometry {
   int64_t ctas;
 };
 
-FwdGeometry fwd_geometry(int64_t S, int64_t BH);
+FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D);
 int fwd_ring_slots(int D);
 cudaError_t launch_sdpa_fwd(const FwdLaunch& launch);
 cudaError_t launch_umma_selftest(const CUtensorMap* a_map, const CUtensorMap* b_map,
