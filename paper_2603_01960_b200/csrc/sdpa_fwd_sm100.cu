@@ -310,14 +310,19 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
           mbar_wait(smem_u32(&bars->p_full[t][h]), uint32_t(j & 1));
           tc_fence_after();
           if (h == kPParts - 1 && lane == 0) rec(t == 0 ? kEvMmaWaitP0 : kEvMmaWaitP1, j);
-          static_assert(kBN / 16 / kPParts == 4, "P part = 4 K-steps of 16 keys");
-          const int ks0 = h * 4;
+          static_assert((kBN / 16 / kPParts) % 4 == 0, "P part = 4k K-steps of 16 keys");
+          constexpr int kSteps = kBN / 16 / kPParts;
 #if TA_MMA_BATCH
-          constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
-          umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks0 * 8,
-                             vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv,
-                             (accumulate || h > 0) ? 1u : 0u);
+#pragma unroll
+          for (int g = 0; g < kSteps / 4; ++g) {
+            const int ks0 = h * kSteps + g * 4;
+            constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
+            umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks0 * 8,
+                               vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv,
+                               (accumulate || ks0 > 0) ? 1u : 0u);
+          }
 #else
+          const int ks0 = h * 4;
           asm volatile("" : "+l"(vd));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
