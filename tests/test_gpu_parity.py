@@ -183,6 +183,28 @@ def test_many_heads_beyond_the_old_grid_y_limit(ta, cuda_device):
         assert (o[b, h].float() - ref).abs().max().item() <= TOL[O.BF16]
 
 
+def test_randomized_shapes_masks_and_scales(ta, cuda_device):
+    # seeded random sweep of the parameter space against the oracle: any B,
+    # H, S in [1, 700], D a multiple of 8 up to 128, both dtypes, all three
+    # masks (padding lengths 0..S), default or explicit scale
+    rng = np.random.default_rng(2603)
+    for case in range(40):
+        B, H = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+        S = int(rng.integers(1, 701))
+        D = int(rng.choice([8, 16, 24, 40, 64, 72, 96, 128]))
+        dt = O.F16 if case % 2 else O.BF16
+        mask = int(rng.integers(0, 3))
+        scale = None if case % 3 else float(rng.uniform(0.02, 0.3))
+        q, k, v = O.make_input((B, H, S, D), dt, 5000 + case)
+        vl = [int(x) for x in rng.integers(0, S + 1, size=B)] if mask == O.MASK_PADDING else None
+        o, lse = run_gpu(ta, q, k, v, dt, scale=scale, causal=mask == O.MASK_CAUSAL,
+                         valid_len=vl)
+        r = oracle_ref(q, k, v, scale=scale, mask_kind=mask, valid_len=vl)
+        ctx = (case, B, H, S, D, dt, mask, scale, vl)
+        assert np.abs(o - r["o"]).max() <= TOL[dt], ctx
+        _check_lse(lse, r["lse"])
+
+
 # ------------------------------------------------- larger S, sampled heads
 @pytest.mark.parametrize("D,dt", [(64, O.BF16), (128, O.BF16), (128, O.F16)])
 def test_long_sequence_sampled_heads(ta, cuda_device, D, dt):
