@@ -255,6 +255,42 @@ def test_bitwise_deterministic(ta, cuda_device):
     assert torch.equal(a, b)
 
 
+def test_concurrent_callers_on_separate_streams(ta, cuda_device):
+    # the C-ABI is reentrant: 4 host threads, each on its own CUDA stream with
+    # its own shape / dtype / mask, reproduce their single-threaded results
+    # bit for bit (plan cache and host workspace are mutex-protected)
+    import threading
+    import torch
+    cases = [((2, 4, 777, 64), torch.bfloat16, False), ((1, 3, 1500, 128), torch.float16, True),
+             ((3, 2, 256, 96), torch.bfloat16, True), ((1, 8, 2048, 128), torch.bfloat16, False)]
+    g = torch.Generator(device="cuda").manual_seed(9)
+    ins = [tuple(torch.randn(*shp, device="cuda", dtype=dt, generator=g) for _ in range(3))
+           for shp, dt, _ in cases]
+    want = [ta.sdpa(*x, causal=c) for x, (_, _, c) in zip(ins, cases)]
+    torch.cuda.synchronize()
+    got = [None] * len(cases)
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(5):
+                    got[i] = ta.sdpa(*ins[i], causal=cases[i][2])
+            s.synchronize()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(cases))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for w, o in zip(want, got):
+        assert torch.equal(w, o)
+
+
 def test_host_entry_matches_device_entry(ta, cuda_device):
     import torch
     q, k, v = O.make_input((1, 2, 700, 128), O.BF16, 4)
