@@ -53,7 +53,7 @@ def _digest() -> str:
 def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
     """Compile (if sources changed) and return the library path.
 
-    ``defines``/``out`` build an experimental variant (e.g. -DTA_EMU_PER8=3)
+    ``defines``/``out`` build an experimental variant (e.g. -DTA_EMU16_D64=6)
     into another file; the product library is the default ``LIB``."""
     LIBDIR.mkdir(exist_ok=True)
     lib = Path(out) if out else LIB

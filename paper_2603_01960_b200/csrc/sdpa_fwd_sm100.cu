@@ -57,10 +57,10 @@ struct Roles {
   // setmaxnreg.inc only draws on registers released by setmaxnreg.dec in
   // the same CTA, so the split must balance around the launch allocation
   // (kQT=2: 65536/384 -> 168, 256*(208-168) == 128*(168-88); kQT=1, two
-  // CTAs: 32768/256 -> 128, 128*(208-128) == 128*(128-48)).
+  // CTAs: 32768/256 -> 128, 128*(200-128) == 128*(128-56)).
   static constexpr int kLaunchRegs = (65536 / (kThreads * kMinBlocks)) & ~7;
-  static constexpr int kRegsSoftmax = 208;
-  static constexpr int kRegsControl = kQT == 1 ? 48 : 88;
+  static constexpr int kRegsSoftmax = kQT == 1 ? 200 : 208;
+  static constexpr int kRegsControl = kQT == 1 ? 56 : 88;
   static_assert(kSoftmaxWarps * 32 * (kRegsSoftmax - kLaunchRegs) <=
                     (kThreads - kSoftmaxWarps * 32) * (kLaunchRegs - kRegsControl),
                 "setmaxnreg.inc would wait forever: register pool does not balance");
@@ -78,16 +78,20 @@ constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
 constexpr float kRescaleThreshold = 8.0f;
-// exp2 work split: of every 8 score columns, kEmuPer8 use the FMA-pipe
-// polynomial (ex2_poly) and the rest the MUFU (measured 16 exp2/clk/SM).
-#ifndef TA_EMU_PER8
-#define TA_EMU_PER8 1
+// exp2 work split: of every 16 score columns, kEmu16 (even: emulated in
+// packed pairs) use the FMA-pipe polynomial (ex2_poly2) and the rest the MUFU
+// (measured 16 exp2/clk/SM).  D=128 is tensor-bound with the softmax on the
+// chain: MUFU only.  D=64 is softmax-throughput bound: 2 of 16 on the FMA
+// pipe (same-box A/B in profiles/r01/microbench.md).
+#ifndef TA_EMU16_D128
+#define TA_EMU16_D128 0
 #endif
-constexpr int kEmuPer8 = TA_EMU_PER8;
-#ifndef TA_EMU_Q3
-#define TA_EMU_Q3 TA_EMU_PER8
+#ifndef TA_EMU16_D64
+#define TA_EMU16_D64 2
 #endif
-constexpr int kEmuQ3 = TA_EMU_Q3;
+#ifndef TA_STALE_D64
+#define TA_STALE_D64 0
+#endif
 // P hand-off granularity to the PV MMAs (2 = halves, 4 = quarters of 32 keys)
 #ifndef TA_P_PARTS
 #define TA_P_PARTS 2
@@ -109,6 +113,11 @@ constexpr float kSumGuard = 256.0f;
 #ifndef TA_SLOTS_D128
 #define TA_SLOTS_D128 4
 #endif
+// D=64, one Q tile per CTA: S rotates through three 64-column TMEM units so
+// that S(j+1) is computed while the softmax works on tile j (below)
+#ifndef TA_D64_ROT
+#define TA_D64_ROT 1
+#endif
 
 template <int D, int kQT = kQTilesFor<D>>
 struct Cfg {
@@ -118,9 +127,32 @@ struct Cfg {
   // K/V ring depth (two CTAs per SM at kQT = 1: 16 KB Q + 4 x 16 KB ring each)
   static constexpr int kSlots = D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128) : kQT == 1 ? 4 : 8;
   static constexpr int kSmemData = kQT * kTileBytes + kSlots * kTileBytes;
-  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/;
+  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/
+#ifdef TA_PAD_SMEM
+      + TA_PAD_SMEM
+#endif
+      ;
+  // S/P rotation (D=64, kQT=1): TMEM units U0 = [0,64), U1 = [64,128),
+  // U2 = [128,192), O at [192,256).  S(j) occupies U0U1 (j even) or U1U2 (j
+  // odd) and P(j) its unit U0 (even) or U2 (odd), so S(j+1) never touches
+  // P(j) and can be issued as soon as the softmax has read S(j).
+  static constexpr bool kRot = TA_D64_ROT && D == 64 && kQT == 1;
+#ifdef TA_ROT_OFIRST
+  static constexpr uint32_t kTmemS = kRot ? 64 : 0;
+  static constexpr uint32_t kTmemO = kRot ? 0 : 128 * kQT;
+#else
   static constexpr uint32_t kTmemS = 0;                  // S_t at col 128 t (fp32)
-  static constexpr uint32_t kTmemO = 128 * kQT;          // O_t at kTmemO + D t (fp32)
+  static constexpr uint32_t kTmemO = kRot ? 192 : 128 * kQT;  // O_t at kTmemO + D t (fp32)
+#endif
+  __device__ static constexpr uint32_t s_col(int j) { return kRot ? 64u * uint32_t(j & 1) : 0u; }
+  __device__ static constexpr uint32_t p_col(int j) { return kRot ? 128u * uint32_t(j & 1) : 0u; }
+  // P hand-off barriers: with the rotation a warp may write P(j+1) before a
+  // slower warp of its warpgroup has written P(j) (S(j+1) only waits for every
+  // warp to have READ S(j)), so even and odd tiles arrive on separate
+  // barriers (p_full[j & 1], phase j / 2); no warp gets two tiles ahead
+  // (S(j+2) waits for PV(j), i.e. for all of P(j)).
+  __device__ static constexpr int p_bar(int t, int j) { return kRot ? (j & 1) : t; }
+  __device__ static constexpr uint32_t p_parity(int j) { return uint32_t(kRot ? (j >> 1) & 1 : j & 1); }
 };
 
 struct Barriers {
@@ -129,6 +161,8 @@ struct Barriers {
   uint64_t p_full[kQTiles][4];  // P key columns [32q, 32q+32) written (q < kPParts)
   uint64_t o_full[kQTiles];
   uint64_t o_half[kQTiles];  // PV(j) over P part 0 complete (stale-max slow path)
+  uint64_t s_read;           // the softmax warps hold S(j) in registers (kRot)
+  uint64_t o_last;           // the last PV complete (kRot: o_full may run ahead)
   uint64_t slot_full[8];
   uint64_t slot_empty[8];
   uint32_t tmem_base;
@@ -146,7 +180,12 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
   // the stale-max softmax pays off where the softmax is on the critical path
   // of a tensor-bound loop (D=128); at D=64 the kernel is softmax-throughput
   // bound and the extra o_half commit costs more than the saved row max
-  constexpr bool kStale = kStaleMax && D == 128;
+  constexpr bool kStale = kStaleMax && (D == 128 || TA_STALE_D64);
+  // the stale-max slow path's o_half parity wait assumes PV(j-1) complete
+  // when S(j) is, which the S/P rotation does not give
+  static_assert(!(kStale && C::kRot), "stale max and the D=64 S/P rotation are exclusive");
+  constexpr int kEmu16 = D == 64 ? TA_EMU16_D64 : TA_EMU16_D128;
+  static_assert(kEmu16 % 2 == 0 && kEmu16 >= 0 && kEmu16 <= 16, "emulated pairs per 16 columns");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -183,15 +222,19 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
     if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
   };
 
+  if (threadIdx.x == 0) rec(kEvKernelStart, 0);
   if (threadIdx.x == kWarpMma * 32) {
     mbar_init(smem_u32(&bars->q_full), 1);
-    for (int t = 0; t < kQT; ++t) {
-      mbar_init(smem_u32(&bars->s_full[t]), 1);
+    for (int t = 0; t < kQTiles; ++t)
       for (int q = 0; q < kPParts; ++q)
         mbar_init(smem_u32(&bars->p_full[t][q]), kBM / 32);  // one arrive per warp
+    for (int t = 0; t < kQT; ++t) {
+      mbar_init(smem_u32(&bars->s_full[t]), 1);
       mbar_init(smem_u32(&bars->o_full[t]), 1);
       mbar_init(smem_u32(&bars->o_half[t]), 1);
     }
+    mbar_init(smem_u32(&bars->s_read), kBM / 32);
+    mbar_init(smem_u32(&bars->o_last), 1);
     for (int s = 0; s < C::kSlots; ++s) {
       mbar_init(smem_u32(&bars->slot_full[s]), 1);
       mbar_init(smem_u32(&bars->slot_empty[s]), 1);
@@ -203,6 +246,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  if (threadIdx.x == 0) rec(kEvKernelStart, 1);
 
   if (warp >= uint32_t(R::kSoftmaxWarps)) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::kRegsControl));
@@ -282,21 +326,21 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
       const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
       const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
       const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
-      auto issue_qk = [&](int t, int r) {
+      auto issue_qk = [&](int t, int r, uint32_t scol = 0) {
         uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
         uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
 #if TA_MMA_BATCH
 #pragma unroll
         for (int r = 0; r < C::kRegions; ++r) {  // 4 K-steps of 16 per 128-B swizzle region
           const uint32_t off = (r * C::kRegionBytes) >> 4;
-          umma_ss_x4<2, 2>(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, r > 0);
+          umma_ss_x4<2, 2>(tmem + C::kTmemS + t * kBN + scol, qd + off, kd + off, idesc_qk, r > 0);
         }
 #else
         asm volatile("" : "+l"(qd), "+l"(kd));
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
-          umma_ss_warp(tmem + C::kTmemS + t * kBN, qd + off, kd + off, idesc_qk, ks > 0);
+          umma_ss_warp(tmem + C::kTmemS + t * kBN + scol, qd + off, kd + off, idesc_qk, ks > 0);
         }
 #endif
         umma_commit_warp(smem_u32(&bars->s_full[t]));
@@ -304,10 +348,11 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
       // PV in two halves of 64 keys, each issued as soon as the softmax
       // warpgroup has written that half of P (P aliases S in TMEM).
       auto issue_pv = [&](int t, int r, bool accumulate, int j) {
+        const uint32_t tP = tmem + C::kTmemS + t * kBN + C::p_col(j);
         uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
 #pragma unroll
         for (int h = 0; h < kPParts; ++h) {
-          mbar_wait(smem_u32(&bars->p_full[t][h]), uint32_t(j & 1));
+          mbar_wait(smem_u32(&bars->p_full[C::p_bar(t, j)][h]), C::p_parity(j));
           tc_fence_after();
           if (h == kPParts - 1 && lane == 0) rec(t == 0 ? kEvMmaWaitP0 : kEvMmaWaitP1, j);
           static_assert((kBN / 16 / kPParts) % 4 == 0, "P part = 4k K-steps of 16 keys");
@@ -317,7 +362,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
           for (int g = 0; g < kSteps / 4; ++g) {
             const int ks0 = h * kSteps + g * 4;
             constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
-            umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks0 * 8,
+            umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tP + ks0 * 8,
                                vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv,
                                (accumulate || ks0 > 0) ? 1u : 0u);
           }
@@ -327,7 +372,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const int ks = ks0 + kk;
-            umma_ts_warp(tmem + C::kTmemO + t * D, tmem + C::kTmemS + t * kBN + ks * 8,
+            umma_ts_warp(tmem + C::kTmemO + t * D, tP + ks * 8,
                          vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
                          (accumulate || ks > 0) ? 1u : 0u);
           }
@@ -338,7 +383,43 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
         if (lane == 0) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
       };
 
-      if constexpr (kQT == 1) {
+      if constexpr (C::kRot) {
+        // S(j+1) as soon as the softmax holds S(j) in registers (its columns
+        // are disjoint from P(j)'s), then PV(j) once P(j) lands
+        const int n = n_kv_t[0];
+        if (n > 0) {
+          mbar_wait(smem_u32(&bars->q_full), 0);
+          tc_fence_after();
+          wait_full(0);
+          issue_qk(0, 0, C::s_col(0));
+          release(0);
+          for (int j = 0; j < n; ++j) {
+#ifdef TA_ROT_LATE
+            {
+              const int rv = 2 * j + 1;
+              wait_full(rv);
+              issue_pv(0, rv, j > 0, j);
+              release(rv);
+            }
+#endif
+            if (j + 1 < n) {
+              const int rk = 2 * (j + 1);
+              mbar_wait(smem_u32(&bars->s_read), uint32_t(j & 1));
+              tc_fence_after();
+              wait_full(rk);
+              issue_qk(0, rk, C::s_col(j + 1));
+              release(rk);
+            }
+#ifndef TA_ROT_LATE
+            const int rv = 2 * j + 1;
+            wait_full(rv);
+            issue_pv(0, rv, j > 0, j);
+            release(rv);
+#endif
+          }
+          umma_commit_warp(smem_u32(&bars->o_last));
+        }
+      } else if constexpr (kQT == 1) {
         // one Q tile: PV(j-1) once P(j-1) lands, then S(j); the tensor core
         // idles through this CTA's softmax, which the other CTA on the SM fills
         const int n = n_kv_t[0];
@@ -400,7 +481,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
     const uint32_t wq = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = int(wq * 32 + lane);
     const uint32_t lane_off = (wq * 32u) << 16;
-    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN;
+    const uint32_t tS0 = tmem + lane_off + C::kTmemS + t * kBN;
     const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
     const float sl2 = args.scale_log2;
     const uint32_t sbar = smem_u32(&bars->s_full[t]);
@@ -415,10 +496,17 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
       tc_fence_after();
       const bool tr = kTrace && row == 0;
       if (tr) rec(kEvSm0SReady + 5 * t, j);
+      const uint32_t tS = tS0 + C::s_col(j);  // S(j)
+      const uint32_t tP = tS0 + C::p_col(j);  // P(j)
       uint32_t sr[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
       tmem_wait_ld();
+      if constexpr (C::kRot) {  // S(j) is in registers: its columns may take S(j+1)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars->s_read));
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
       if (tr) rec(kEvSm0Loaded + 5 * t, j);
@@ -482,12 +570,10 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
       }
       float m_use = m_run == -INFINITY ? 0.f : m_run;
       // x = s * scale*log2e - m as packed FFMA2; exp2 split between the MUFU
-      // and the FMA pipe (kEmuPer8 of every 8 columns, emulated in pairs);
+      // and the FMA pipe (kEmu16 of every 16 columns, emulated in pairs);
       // row sum as packed FADD2 into 4 pair accumulators.
       const uint64_t sl2x2 = f2(sl2, sl2);
-      // exps of the row in kPParts parts; E of every 8 columns on the FMA pipe
-      auto exps = [&](auto emu) {
-      constexpr int E = decltype(emu)::value;
+      // exps of the row in kPParts parts
 #pragma unroll
       for (int h = 0; h < kPParts; ++h) {
         constexpr int kCols = kBN / kPParts;  // key columns per P part
@@ -504,7 +590,9 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
           for (int u = 0; u < 4; ++u)
             x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
           float p[8];
-          // emulated pairs are the last kEmuPer8/2 pairs of the group
+          // emulated pairs are the last ones of the group: of the kEmu16/2
+          // pairs per 16 columns, even groups take the larger half
+          const int emu_pairs = (g & 1) ? kEmu16 / 4 : kEmu16 / 2 - kEmu16 / 4;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
 #ifdef TA_DEBUG_NO_EXP  // timing ablation only: wrong results
@@ -512,7 +600,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
               f2_split(x[u], p[2 * u], p[2 * u + 1]);
             } else
 #endif
-            if (2 * u >= 8 - E) {
+            if (u >= 4 - emu_pairs) {
               ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
             } else {
               float a, b;
@@ -580,30 +668,28 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
         }
         l_run += psum;
 #pragma unroll
-        for (int i = 0; i < kCols / 32; ++i) tmem_st16(tS + h * (kCols / 2) + i * 16, pk[i]);
+        for (int i = 0; i < kCols / 32; ++i) tmem_st16(tP + h * (kCols / 2) + i * 16, pk[i]);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[t][h]));
+        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[C::p_bar(t, j)][h]));
         if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
         if (kTrace && h == kPParts - 1 && t == 0 && wq > 0 && lane == 0)
           rec(kEvSm0ArriveW1 + int(wq) - 1, j);
       }
-      };
-      // the MMA warp shares SMSP 3 (lane quadrant 3): its softmax warps trade
-      // FMA-pipe emulation (issue slots) for MUFU time
-      if (kEmuQ3 != kEmuPer8 && wq == 3)
-        exps(std::integral_constant<int, kEmuQ3>{});
-      else
-        exps(std::integral_constant<int, kEmuPer8>{});
       if (tr) rec(kEvSm0PArrive + 5 * t, j);
     }
 
     // ------------------------------------------------------------- epilogue
     // rows with no admitted key (padding valid_len == 0) are exact zeros
     // with LSE = -inf (finalize, tiled.hpp:231-233); their O was never written
+    // (kRot: when the softmax finishes, S(n-1) done only implies PV(n-3)
+    // done, so o_full's phase parity is ambiguous; o_last completes once)
     if (my_n_kv > 0) {
-      mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
+      if constexpr (C::kRot)
+        mbar_wait(smem_u32(&bars->o_last), 0u);
+      else
+        mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
       tc_fence_after();
     }
     const int grow = q0 + t * kBM + row;
@@ -638,6 +724,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
     if (args.lse != nullptr && grow < S)
       args.lse[size_t(bh) * S + grow] =
           l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+    if (kTrace && row == 0) rec(kEvEpilogueDone, t);
   }
 
   tc_fence_before();
