@@ -24,6 +24,9 @@ print("iter " + " ".join(f"{x:>9s}" for x in names))
 for j in range(n):
     print(f"{j:4d} " + " ".join(f"{(t[e, j] - base) if t[e, j] else 0:9d}" for e in range(18)))
 import numpy as np
+print(f"kernel start {t[21, 0] - base}, after setup {t[21, 1] - base}, "
+      f"epilogue done tile0 {t[22, 0] - base} tile1 {t[22, 1] - base}, "
+      f"last P arrive tile1 {t[13, min(n, 64) - 1] - base}")
 js = range(8, n - 1)
 def d(a, b): return np.mean([t[b, j] - t[a, j] for j in js])
 print("mean over iters 8..n-2 (cycles):")
