@@ -355,28 +355,33 @@ def run_sweep(args):
         is_causal = name.endswith("causal")
         q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=dt) for _ in range(3))
         o = torch.empty_like(q)
-        for _ in range(3):
-            ta.sdpa(q, k, v, out=o, causal=is_causal)
-        torch.cuda.synchronize()
-        n = 3 if S >= 32768 else 20
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(n):
-            ta.sdpa(q, k, v, out=o, causal=is_causal)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / n
+
+        def timed(fn):
+            # warm up for >= 0.2 s (clocks settle under the power cap after
+            # the previous config), then time >= 0.2 s of back-to-back calls
+            fn()
+            torch.cuda.synchronize()
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            n = max(3, int(200.0 / max(e0.elapsed_time(e1), 1e-3)))
+            for _ in range(n):
+                fn()
+            e0.record()
+            for _ in range(n):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / n
+
+        ms = timed(lambda: ta.sdpa(q, k, v, out=o, causal=is_causal))
         tf = flops(B, H, S, D) / ms / 1e9
         ref_ms = None
         if args.vendor:
-            for _ in range(2):
-                torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=is_causal)
-            e0.record()
-            for _ in range(n):
-                torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=is_causal)
-            e1.record()
-            torch.cuda.synchronize()
-            ref_ms = e0.elapsed_time(e1) / n
+            ref_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(
+                q, k, v, is_causal=is_causal))
         rows.append(dict(config=name, ms=ms, tflops=tf, frac=tf / pk["bf16_tflops"],
                          causal_effective_tflops=tf / 2 if is_causal else None,
                          hbm_gbs=(8 * B * H * S * D + 4 * B * H * S) / ms / 1e6,

@@ -81,16 +81,13 @@ constexpr float kRescaleThreshold = 8.0f;
 // exp2 work split: of every 16 score columns, kEmu16 (even: emulated in
 // packed pairs) use the FMA-pipe polynomial (ex2_poly2) and the rest the MUFU
 // (measured 16 exp2/clk/SM).  D=128 is tensor-bound with the softmax on the
-// chain: MUFU only.  D=64 is softmax-throughput bound: 2 of 16 on the FMA
+// chain: MUFU only.  D=64 is softmax-throughput bound: 4 of 16 on the FMA
 // pipe (same-box A/B in profiles/r01/microbench.md).
 #ifndef TA_EMU16_D128
 #define TA_EMU16_D128 0
 #endif
 #ifndef TA_EMU16_D64
-#define TA_EMU16_D64 2
-#endif
-#ifndef TA_STALE_D64
-#define TA_STALE_D64 0
+#define TA_EMU16_D64 4
 #endif
 // P hand-off granularity to the PV MMAs (2 = halves, 4 = quarters of 32 keys)
 #ifndef TA_P_PARTS
@@ -113,6 +110,12 @@ constexpr float kSumGuard = 256.0f;
 #ifndef TA_SLOTS_D128
 #define TA_SLOTS_D128 4
 #endif
+#ifndef TA_TRACE_ROW  // row whose softmax phases the diagnostic trace records
+#define TA_TRACE_ROW 0
+#endif
+#ifndef TA_SLOTS_D64
+#define TA_SLOTS_D64 4
+#endif
 // D=64, one Q tile per CTA: S rotates through three 64-column TMEM units so
 // that S(j+1) is computed while the softmax works on tile j (below)
 #ifndef TA_D64_ROT
@@ -125,7 +128,7 @@ struct Cfg {
   static constexpr int kTileBytes = kBM * D * 2;            // one Q / K / V tile
   static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
   // K/V ring depth (two CTAs per SM at kQT = 1: 16 KB Q + 4 x 16 KB ring each)
-  static constexpr int kSlots = D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128) : kQT == 1 ? 4 : 8;
+  static constexpr int kSlots = D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128) : kQT == 1 ? TA_SLOTS_D64 : 8;
   static constexpr int kSmemData = kQT * kTileBytes + kSlots * kTileBytes;
   static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/
 #ifdef TA_PAD_SMEM
@@ -177,13 +180,10 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
   using R = Roles<kQT>;
   constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
                 kWarpMma = R::kWarpMma;
-  // the stale-max softmax pays off where the softmax is on the critical path
-  // of a tensor-bound loop (D=128); at D=64 the kernel is softmax-throughput
-  // bound and the extra o_half commit costs more than the saved row max
-  constexpr bool kStale = kStaleMax && (D == 128 || TA_STALE_D64);
-  // the stale-max slow path's o_half parity wait assumes PV(j-1) complete
-  // when S(j) is, which the S/P rotation does not give
-  static_assert(!(kStale && C::kRot), "stale max and the D=64 S/P rotation are exclusive");
+  // stale max at both head dims: it takes the row max (and its latency)
+  // off the softmax of every K/V tile after the first (D=128 +2.3%, D=64
+  // with the S/P rotation +4.5%, same-box A/B)
+  constexpr bool kStale = kStaleMax;
   constexpr int kEmu16 = D == 64 ? TA_EMU16_D64 : TA_EMU16_D128;
   static_assert(kEmu16 % 2 == 0 && kEmu16 >= 0 && kEmu16 <= 16, "emulated pairs per 16 columns");
   extern __shared__ uint8_t smem_raw[];
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
       uint32_t phase = 0;
       for (int j = 0; j < n_kv; ++j) {
         for (int kv = 0; kv < 2; ++kv) {
-          mbar_wait(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
+          mbar_wait_ctrl(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
           const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
           mbar_arrive_expect_tx(fbar, C::kTileBytes);
           const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
       auto slot_of = [](int r) { return r % C::kSlots; };
       auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
       auto wait_full = [&](int r) {
-        mbar_wait(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
+        mbar_wait_ctrl(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
         tc_fence_after();
       };
       auto release = [&](int r) { umma_commit_warp(smem_u32(&bars->slot_empty[slot_of(r)])); };
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
         uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
 #pragma unroll
         for (int h = 0; h < kPParts; ++h) {
-          mbar_wait(smem_u32(&bars->p_full[C::p_bar(t, j)][h]), C::p_parity(j));
+          mbar_wait_ctrl(smem_u32(&bars->p_full[C::p_bar(t, j)][h]), C::p_parity(j));
           tc_fence_after();
           if (h == kPParts - 1 && lane == 0) rec(t == 0 ? kEvMmaWaitP0 : kEvMmaWaitP1, j);
           static_assert((kBN / 16 / kPParts) % 4 == 0, "P part = 4k K-steps of 16 keys");
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
 #endif
             if (j + 1 < n) {
               const int rk = 2 * (j + 1);
-              mbar_wait(smem_u32(&bars->s_read), uint32_t(j & 1));
+              mbar_wait_ctrl(smem_u32(&bars->s_read), uint32_t(j & 1));
               tc_fence_after();
               wait_full(rk);
               issue_qk(0, rk, C::s_col(j + 1));
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
     for (int j = 0; j < my_n_kv; ++j) {
       mbar_wait(sbar, uint32_t(j & 1));
       tc_fence_after();
-      const bool tr = kTrace && row == 0;
+      const bool tr = kTrace && row == TA_TRACE_ROW;
       if (tr) rec(kEvSm0SReady + 5 * t, j);
       const uint32_t tS = tS0 + C::s_col(j);  // S(j)
       const uint32_t tP = tS0 + C::p_col(j);  // P(j)
@@ -643,10 +643,10 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
             m_run = m_part;
             m_use = m_run;
           }
-          if (h == 0)
-            mbar_wait(obar, uint32_t((j - 1) & 1));
-          else
-            mbar_wait(smem_u32(&bars->o_half[t]), uint32_t(j & 1));
+          // (with the S/P rotation S(j) done only implies PV(j-2) done:
+          // PV(j-1) complete first makes the o_half parity unambiguous)
+          if (h == 0 || C::kRot) mbar_wait(obar, uint32_t((j - 1) & 1));
+          if (h != 0) mbar_wait(smem_u32(&bars->o_half[t]), uint32_t(j & 1));
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < D / 16; ++c) {

@@ -136,9 +136,9 @@ def test_large_scores_exercise_lazy_rescale(ta, cuda_device):
 def test_running_max_jumps_in_later_halves(ta, cuda_device, dt):
     # Scores stay small except planted keys aligned with q, each exceeding
     # the running max by > 2^8 (log2 units) in the first or second half of a
-    # later K/V tile: drives every branch of the lazy rescale (the D=128
-    # stale-max slow path for half 0 and half 1, and the exact-max path at
-    # D=64) against the oracle.
+    # later K/V tile: drives every branch of the lazy rescale (the stale-max
+    # slow path for half 0 and half 1 at both head dims; at D=64 under the
+    # S/P rotation, where PV(j-1) may still be in flight) against the oracle.
     for D in (64, 128):
         q, k, v = O.make_input((1, 4, 512, D), dt, 91)
         q = np.full_like(q, 0.5)          # every row = 0.5 * ones (on the 16-bit grid)
