@@ -32,6 +32,14 @@ def d(a, b): return np.mean([t[b, j] - t[a, j] for j in js])
 print("mean over iters 8..n-2 (cycles):")
 print(" period s0Ready->s0Ready", np.mean([t[4, j + 1] - t[4, j] for j in js]))
 print(" s0: ready->load %.0f load->max %.0f max->exp %.0f exp->arrive %.0f" % (d(4, 5), d(5, 6), d(6, 7), d(7, 8)))
+print(" s0: arrive(j) -> ready(j+1) %.0f" % np.mean([t[4, j + 1] - t[8, j] for j in js]))
+if t[2, 8] and not t[9, 8]:  # one Q tile per CTA (D=64): MMA-warp view of S(j+1)
+    print(" QT=1: ready(j) -> mma sees s_read(j) %.0f, -> S(j+1) issued %.0f, -> S(j+1) done %.0f, "
+          "mma issued PV(j) -> S(j+1) issued %.0f" % (
+              np.mean([t[2, j] - t[4, j] for j in js]), np.mean([t[3, j] - t[4, j] for j in js]),
+              np.mean([t[15, j + 1] - t[4, j] for j in js]), np.mean([t[3, j + 1] - t[1, j] for j in js])))
+    print(" QT=1: last warp arrive(j) = max(w0..w3) -> mma sees P(j) %.0f" % np.mean(
+        [t[0, j] - max(t[8, j], *(t[17 + w, j] for w in (1, 2, 3))) for j in js]))
 print(" s1: ready->load %.0f load->max %.0f max->exp %.0f exp->arrive %.0f" % (d(9, 10), d(10, 11), d(11, 12), d(12, 13)))
 print(" tile-0 warp skew (warp w arrive - warp 0 arrive) w=1,2,3:", [np.mean([t[17 + w, j] - t[8, j] for j in js]) for w in (1, 2, 3)])
 print(" s0 arrive(j) -> mma sees P0(j):", np.mean([t[0, j] - t[8, j] for j in js]))
