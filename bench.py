@@ -340,7 +340,7 @@ def run_sweep(args):
         ("cfg1 B1 H8 S512 D64 f16", 1, 8, 512, 64, torch.float16),
         *[(f"S-sweep B4 H16 S{s} D64 bf16", 4, 16, s, 64, torch.bfloat16)
           for s in (1024, 2048, 4096, 8192, 16384)],
-        *[(f"D-sweep B8 H32 S4096 D{d} {n}", 8, 32, 4096, d, t) for d in (64, 96, 128)
+        *[(f"D-sweep B8 H32 S4096 D{d} {n}", 8, 32, 4096, d, t) for d in (64, 96, 128, 160, 256)
           for n, t in (("f16", torch.float16), ("bf16", torch.bfloat16))],
         ("ViT B64 H16 S1024 D64 bf16", 64, 16, 1024, 64, torch.bfloat16),
         ("long B8 H64 S32768 D128 bf16", 8, 64, 32768, 128, torch.bfloat16),
