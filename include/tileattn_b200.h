@@ -66,9 +66,10 @@ typedef struct ta_schedule {
   int32_t layout;
 } ta_schedule;
 
-/* Shape (types.hpp:27-36): [B,H,S,D] row-major, D innermost.  The kernel
- * covers D a multiple of 8 up to 128 (D <= 64 on the D=64 kernel, else the
- * D=128 kernel with TMA zero-fill past D); other D -> TA_ERR_UNSUPPORTED. */
+/* Shape (types.hpp:27-36): [B,H,S,D] row-major, D innermost.  The kernels
+ * cover D a multiple of 8 up to 256 (D runs on the 64 / 128 / 192 / 256-column
+ * instantiation that holds it, TMA zero-fill past D); other D ->
+ * TA_ERR_UNSUPPORTED. */
 typedef struct ta_shape {
   int64_t b, h, s, d;
 } ta_shape;

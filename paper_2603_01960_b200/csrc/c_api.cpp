@@ -85,18 +85,19 @@ ta_status validate_device_support(ta_shape sh, ta_dtype dt, ta_mask_kind mask) {
   if (dt == TA_F32)
     return fail(TA_ERR_UNSUPPORTED, "dtype f32 is not a tensor-core input; use f16 or bf16");
   if (dt != TA_F16 && dt != TA_BF16) return fail(TA_ERR_INVALID_ARGUMENT, "unknown dtype");
-  // D <= 64 runs the D=64 kernel, 64 < D <= 128 the D=128 kernel: the TMA
-  // boxes zero-fill the columns past D (they add nothing to Q.K^T and give
-  // zero O columns, which are not stored).  Rows must be 16-B aligned for TMA.
-  if (sh.d > 128 || sh.d % 8 != 0)
+  // D runs on the smallest kernel of 64 / 128 / 192 / 256 columns that
+  // holds it: the TMA boxes zero-fill the columns past D (they add nothing to
+  // Q.K^T and give zero O columns, which are not stored).  Rows must be 16-B
+  // aligned for TMA.  D > 256 would need more than the 512 TMEM columns.
+  if (sh.d > 256 || sh.d % 8 != 0)
     return fail(TA_ERR_UNSUPPORTED, "head dim " + std::to_string(sh.d) +
-                                        " not supported (D a multiple of 8, D <= 128)");
+                                        " not supported (D a multiple of 8, D <= 256)");
   if (mask == TA_MASK_PADDING && sh.b > ta::kMaxPaddingBatch)
     return fail(TA_ERR_UNSUPPORTED, "padding masks support B <= " +
                                         std::to_string(ta::kMaxPaddingBatch));
   if (sh.s > (int64_t(1) << 30)) return fail(TA_ERR_UNSUPPORTED, "S too large");
-  if (((sh.s + 255) / 256) * sh.b * sh.h > 0x7FFFFFFF)
-    return fail(TA_ERR_UNSUPPORTED, "more than 2^31 - 1 work items (B*H*ceil(S/256))");
+  if (ta::fwd_geometry(sh.s, sh.b * sh.h, sh.d).ctas > 0x7FFFFFFF)
+    return fail(TA_ERR_UNSUPPORTED, "more than 2^31 - 1 CTAs (B*H*ceil(S/rows per CTA))");
   return TA_OK;
 }
 
@@ -277,7 +278,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
     for (int64_t b = 0; b < mask_args.batches; ++b)
       L.args.valid_len[b] = int(mask_args.valid_len[b]);
   L.bh = bh;
-  L.head_dim = sh.d <= 64 ? 64 : 128;  // kernel instantiation
+  L.head_dim = ta::fwd_kernel_head_dim(sh.d);  // kernel instantiation
   L.args.head_dim = int(sh.d);         // row length of q/k/v/o in memory
   L.bf16 = bf16;
   L.stream = stream;

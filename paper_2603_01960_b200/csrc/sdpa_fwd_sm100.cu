@@ -44,23 +44,26 @@ constexpr int kQTiles = 2;      // max Q tiles per CTA (ping-pong)
 // loop).  Softmax warps 4t..4t+3 own Q tile t (warp w <-> TMEM lane quadrant
 // w % 4); the control warps take the top ids (the SM's warp arbiter favours
 // high ids, so the single-thread roles are never starved).
-template <int kQT>
+// kWide (D > 128): one Q tile, one CTA per SM (the O accumulator needs up
+// to 256 TMEM columns), no register rebalancing (255 registers per thread).
+template <int kQT, bool kWide = false>
 struct Roles {
   static constexpr int kSoftmaxWarps = 4 * kQT;
   static constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
-  static constexpr int kMinBlocks = kQT == 1 ? 2 : 1;
+  static constexpr int kMinBlocks = kQT == 1 && !kWide ? 2 : 1;
+  static constexpr bool kSetMaxNReg = !kWide;
   static constexpr int kWarpAlloc = kSoftmaxWarps + 0;  // TMEM allocator (otherwise idle)
   static constexpr int kWarpTma = kSoftmaxWarps + 1;
   static constexpr int kWarpTrace = kSoftmaxWarps + 2;  // diagnostics only
   static constexpr int kWarpMma = kSoftmaxWarps + 3;
-  static constexpr uint32_t kTmemCols = kQT == 1 ? 256 : 512;
+  static constexpr uint32_t kTmemCols = kQT == 1 && !kWide ? 256 : 512;
   // setmaxnreg.inc only draws on registers released by setmaxnreg.dec in
   // the same CTA, so the split must balance around the launch allocation
   // (kQT=2: 65536/384 -> 168, 256*(208-168) == 128*(168-88); kQT=1, two
   // CTAs: 32768/256 -> 128, 128*(200-128) == 128*(128-56)).
-  static constexpr int kLaunchRegs = (65536 / (kThreads * kMinBlocks)) & ~7;
-  static constexpr int kRegsSoftmax = kQT == 1 ? 200 : 208;
-  static constexpr int kRegsControl = kQT == 1 ? 56 : 88;
+  static constexpr int kLaunchRegs = kWide ? 248 : (65536 / (kThreads * kMinBlocks)) & ~7;
+  static constexpr int kRegsSoftmax = kWide ? 248 : kQT == 1 ? 200 : 208;
+  static constexpr int kRegsControl = kWide ? 248 : kQT == 1 ? 56 : 88;
   static_assert(kSoftmaxWarps * 32 * (kRegsSoftmax - kLaunchRegs) <=
                     (kThreads - kSoftmaxWarps * 32) * (kLaunchRegs - kRegsControl),
                 "setmaxnreg.inc would wait forever: register pool does not balance");
@@ -73,7 +76,9 @@ struct Roles {
 #define TA_D128_TILES 2
 #endif
 template <int D>
-constexpr int kQTilesFor = D == 64 ? TA_D64_TILES : TA_D128_TILES;
+constexpr int kQTilesFor = D == 64 ? TA_D64_TILES : D == 128 ? TA_D128_TILES : 1;
+template <int D, int kQT>
+using RolesFor = Roles<kQT, (D > 128)>;
 constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
@@ -128,7 +133,10 @@ struct Cfg {
   static constexpr int kTileBytes = kBM * D * 2;            // one Q / K / V tile
   static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
   // K/V ring depth (two CTAs per SM at kQT = 1: 16 KB Q + 4 x 16 KB ring each)
-  static constexpr int kSlots = D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128) : kQT == 1 ? TA_SLOTS_D64 : 8;
+  // (D > 128: Q + 3 x 48 KB or 2 x 64 KB = 192 KB, one CTA per SM)
+  static constexpr int kSlots = D > 128 ? (D == 192 ? 3 : 2)
+                                : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128)
+                                : kQT == 1 ? TA_SLOTS_D64 : 8;
   static constexpr int kSmemData = kQT * kTileBytes + kSlots * kTileBytes;
   static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/
 #ifdef TA_PAD_SMEM
@@ -139,7 +147,7 @@ struct Cfg {
   // U2 = [128,192), O at [192,256).  S(j) occupies U0U1 (j even) or U1U2 (j
   // odd) and P(j) its unit U0 (even) or U2 (odd), so S(j+1) never touches
   // P(j) and can be issued as soon as the softmax has read S(j).
-  static constexpr bool kRot = TA_D64_ROT && D == 64 && kQT == 1;
+  static constexpr bool kRot = TA_D64_ROT && kQT == 1 && (D == 64 || D > 128);
 #ifdef TA_ROT_OFIRST
   static constexpr uint32_t kTmemS = kRot ? 64 : 0;
   static constexpr uint32_t kTmemO = kRot ? 0 : 128 * kQT;
@@ -172,12 +180,12 @@ struct Barriers {
 };
 
 template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>>
-__global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
+__global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::kMinBlocks)
     sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
   using C = Cfg<D, kQT>;
-  using R = Roles<kQT>;
+  using R = RolesFor<D, kQT>;
   constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
                 kWarpMma = R::kWarpMma;
   // stale max at both head dims: it takes the row max (and its latency)
@@ -249,7 +257,8 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
   if (threadIdx.x == 0) rec(kEvKernelStart, 1);
 
   if (warp >= uint32_t(R::kSoftmaxWarps)) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::kRegsControl));
+    if constexpr (R::kSetMaxNReg)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::kRegsControl));
   if (warp == kWarpTma) {
     // ------------------------------------------------------------------ TMA
     if (lane == 0) {
@@ -476,7 +485,8 @@ __global__ void __launch_bounds__(Roles<kQT>::kThreads, Roles<kQT>::kMinBlocks)
   }
   } else {
     // -------------------------------------------------------------- softmax
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R::kRegsSoftmax));
+    if constexpr (R::kSetMaxNReg)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R::kRegsSoftmax));
     const int t = int(warp) / 4;
     const uint32_t wq = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = int(wq * 32 + lane);
@@ -841,7 +851,7 @@ cudaError_t launch_typed(const FwdLaunch& L) {
   const int64_t ctas = int64_t((L.args.seq_len + rows_per_cta - 1) / rows_per_cta) * L.bh;
   if (ctas > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned int>(ctas), 1u, 1u);
-  kern<<<grid, Roles<kQT>::kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+  kern<<<grid, RolesFor<D, kQT>::kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
       *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
   return cudaGetLastError();
 }
@@ -849,7 +859,7 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 }  // namespace
 
 FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D) {
-  const int qt = D <= 64 ? kQTilesFor<64> : kQTilesFor<128>;  // NOLINT
+  const int qt = D <= 64 ? kQTilesFor<64> : D <= 128 ? kQTilesFor<128> : 1;  // NOLINT
   FwdGeometry g;
   g.block_m = kBM;
   g.block_n = kBN;
@@ -860,12 +870,17 @@ FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D) {
 }
 
 int fwd_ring_slots(int D) {
-  return D > 64 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
+  return D > 192 ? Cfg<256>::kSlots : D > 128 ? Cfg<192>::kSlots
+         : D > 64 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
 }
+
+int fwd_kernel_head_dim(int64_t D) { return D <= 64 ? 64 : D <= 128 ? 128 : D <= 192 ? 192 : 256; }
 
 cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
   if (L.head_dim == 128) return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
   if (L.head_dim == 64) return L.bf16 ? launch_typed<64, true>(L) : launch_typed<64, false>(L);
+  if (L.head_dim == 192) return L.bf16 ? launch_typed<192, true>(L) : launch_typed<192, false>(L);
+  if (L.head_dim == 256) return L.bf16 ? launch_typed<256, true>(L) : launch_typed<256, false>(L);
   return cudaErrorInvalidValue;
 }
 

@@ -80,6 +80,9 @@ struct FwdGeometry {
 
 FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D);
 int fwd_ring_slots(int D);
+// kernel instantiation for a head dim: 64, 128, 192 or 256 (memory D <= it;
+// the TMA boxes zero-fill the extra columns)
+int fwd_kernel_head_dim(int64_t D);
 cudaError_t launch_sdpa_fwd(const FwdLaunch& launch);
 cudaError_t launch_umma_selftest(const CUtensorMap* a_map, const CUtensorMap* b_map,
                                  const void* a_glob, float* d_out, int mode, bool bf16,

@@ -125,7 +125,7 @@ static void test_validation_order_and_classes() {  // tiled.cpp:256-259, types.c
   const AttnInput f32 = make_input(Shape{1, 1, 32, 64}, DType::F32, 1);
   CHECK_THROWS_AS(sdpa_tiled(f32, MaskSpec::none(), ScaleSpec{}, TileSchedule{}, cache),
                   UnsupportedScheduleError);
-  for (int64_t d : {44, 160}) {  // not a multiple of 8 / above 128
+  for (int64_t d : {44, 264}) {  // not a multiple of 8 / above 256
     const AttnInput odd = make_input(Shape{1, 2, 32, d}, DType::BF16Emu, 77);
     CHECK_THROWS_AS(sdpa_tiled(odd, MaskSpec::none(), ScaleSpec{}, TileSchedule{}, cache),
                     UnsupportedScheduleError);

@@ -92,7 +92,7 @@ def test_validation_order_and_error_classes():
     with pytest.raises(ta.UnsupportedScheduleError):
         _call(shape=(1, 1, 64, 44))
     with pytest.raises(ta.UnsupportedScheduleError):
-        _call(shape=(1, 1, 64, 160))
+        _call(shape=(1, 1, 64, 264))
 
 
 def test_no_cpu_fallback_without_device():

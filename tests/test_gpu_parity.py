@@ -156,10 +156,11 @@ def test_running_max_jumps_in_later_halves(ta, cuda_device, dt):
 
 # ------------------------------------------- head dims other than 64 / 128
 @pytest.mark.parametrize("dt", [O.BF16, O.F16])
-@pytest.mark.parametrize("D", [8, 32, 48, 80, 96, 120])
+@pytest.mark.parametrize("D", [8, 32, 48, 80, 96, 120, 136, 160, 192, 200, 256])
 def test_other_head_dims_match_oracle(ta, cuda_device, dt, D):
-    # D <= 64 runs the D=64 kernel, D <= 128 the D=128 kernel, the columns
-    # past D zero-filled by TMA (the paper's grid has D=96)
+    # D runs on the 64 / 128 / 192 / 256-column kernel that holds it, the
+    # columns past D zero-filled by TMA (the paper's grid has D=96 and D=160;
+    # SURVEY.md 8f)
     q, k, v = O.make_input((2, 2, 300, D), dt, 1000 + D)
     for causal in (False, True):
         o, lse = run_gpu(ta, q, k, v, dt, causal=causal)
@@ -314,7 +315,7 @@ def test_stats_report_executed_tiling(ta, cuda_device):
 
 def test_errors_are_loud(ta, cuda_device):
     import torch
-    for d in (44, 160):  # not a multiple of 8 / above the TMEM budget
+    for d in (44, 264):  # not a multiple of 8 / above the TMEM budget
         x = torch.zeros(1, 1, 64, d, device="cuda", dtype=torch.bfloat16)
         with pytest.raises(ta.UnsupportedScheduleError):
             ta.sdpa(x, x, x)

@@ -60,16 +60,16 @@ def test_b200_method_fails_loudly_without_a_device(tmp_path):
 @pytest.mark.gpu
 @needs_grid
 def test_b200_method_in_the_reference_grid(tmp_path, cuda_device):
-    r, out = run_grid(tmp_path, "--methods", "b200,tiled", "--s", "128,512", "--d", "64,96,160",
+    r, out = run_grid(tmp_path, "--methods", "b200,tiled", "--s", "128,512", "--d", "64,96,160,264",
                       "--dtypes", "f16,bf16", "--masks", "none,causal", "--b", "1", "--h", "2",
                       "--warmup", "1", "--timed", "3")
     assert r.returncode == 0, r.stderr
     rows = read(out)
-    assert len(rows) == 2 * 2 * 3 * 2 * 2
+    assert len(rows) == 2 * 2 * 4 * 2 * 2
     ours = [x for x in rows if x["method"] == "b200"]
     ref = {(x["S"], x["D"], x["dtype"], x["causal"]): x for x in rows if x["method"] == "tiled"}
     for x in ours:
-        if x["D"] == "160":  # beyond the kernel's TMEM budget: the harness's unsupported row
+        if x["D"] == "264":  # beyond the kernels' TMEM budget: the harness's unsupported row
             assert x["status"] == "unsupported" and x["median_ms"] == "NaN"
             continue
         assert x["status"] == "ok", x  # passed the reference's correctness gate
