@@ -138,23 +138,19 @@ struct Cfg {
                                 : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128)
                                 : kQT == 1 ? TA_SLOTS_D64 : 8;
   static constexpr int kSmemData = kQT * kTileBytes + kSlots * kTileBytes;
-  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/
-#ifdef TA_PAD_SMEM
-      + TA_PAD_SMEM
-#endif
-      ;
+  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/;
   // S/P rotation (D=64, kQT=1): TMEM units U0 = [0,64), U1 = [64,128),
   // U2 = [128,192), O at [192,256).  S(j) occupies U0U1 (j even) or U1U2 (j
   // odd) and P(j) its unit U0 (even) or U2 (odd), so S(j+1) never touches
   // P(j) and can be issued as soon as the softmax has read S(j).
   static constexpr bool kRot = TA_D64_ROT && kQT == 1 && (D == 64 || D > 128);
-#ifdef TA_ROT_OFIRST
-  static constexpr uint32_t kTmemS = kRot ? 64 : 0;
-  static constexpr uint32_t kTmemO = kRot ? 0 : 128 * kQT;
-#else
+  // ring filled in the rotation's consumption order (K_{j+1} before V_j):
+  // with the 2-3 slot rings of D > 128 the next K no longer waits behind a V
+  // slot that frees only when PV completes (+32-36% at D=160/256; D=64 with
+  // 4 slots gains nothing and keeps the plain order)
+  static constexpr bool kConsumeOrder = kRot && D > 128;
   static constexpr uint32_t kTmemS = 0;                  // S_t at col 128 t (fp32)
   static constexpr uint32_t kTmemO = kRot ? 192 : 128 * kQT;  // O_t at kTmemO + D t (fp32)
-#endif
   __device__ static constexpr uint32_t s_col(int j) { return kRot ? 64u * uint32_t(j & 1) : 0u; }
   __device__ static constexpr uint32_t p_col(int j) { return kRot ? 128u * uint32_t(j & 1) : 0u; }
   // P hand-off barriers: with the rotation a warp may write P(j+1) before a
@@ -276,20 +272,41 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
 #endif
       int slot = 0;
       uint32_t phase = 0;
-      for (int j = 0; j < n_kv; ++j) {
-        for (int kv = 0; kv < 2; ++kv) {
+      if constexpr (!C::kConsumeOrder) {
+        // ring positions: K_j at 2j, V_j at 2j+1
+        for (int j = 0; j < n_kv; ++j) {
+          for (int kv = 0; kv < 2; ++kv) {
+            mbar_wait_ctrl(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
+            const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+            mbar_arrive_expect_tx(fbar, C::kTileBytes);
+            const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
+            for (int r = 0; r < C::kRegions; ++r)
+#if TA_KV_EVICT_LAST
+              tma_load_3d_hint(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar,
+                               r * 64, j * kBN, bh, kv_policy);
+#else
+              tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
+                          j * kBN, bh);
+#endif
+            if (++slot == C::kSlots) {
+              slot = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      } else {
+        // the order the rotation consumes them: K_0, K_1, V_0, K_2, V_1, ...,
+        // K_{n-1}, V_{n-2}, V_{n-1} (position p -> tile)
+        for (int p = 0; p < 2 * n_kv; ++p) {
+          const bool is_k = p == 0 || (p != 2 * n_kv - 1 && (p & 1));
+          const int j = p == 0 ? 0 : p == 2 * n_kv - 1 ? n_kv - 1 : (p & 1) ? (p + 1) >> 1 : (p - 2) >> 1;
           mbar_wait_ctrl(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
           const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
           mbar_arrive_expect_tx(fbar, C::kTileBytes);
-          const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
+          const CUtensorMap* map = is_k ? &tmap_k : &tmap_v;
           for (int r = 0; r < C::kRegions; ++r)
-#if TA_KV_EVICT_LAST
-            tma_load_3d_hint(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
-                             j * kBN, bh, kv_policy);
-#else
             tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
                         j * kBN, bh);
-#endif
           if (++slot == C::kSlots) {
             slot = 0;
             phase ^= 1;
@@ -403,28 +420,23 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
           issue_qk(0, 0, C::s_col(0));
           release(0);
           for (int j = 0; j < n; ++j) {
-#ifdef TA_ROT_LATE
-            {
-              const int rv = 2 * j + 1;
-              wait_full(rv);
-              issue_pv(0, rv, j > 0, j);
-              release(rv);
-            }
-#endif
             if (j + 1 < n) {
-              const int rk = 2 * (j + 1);
+              // K_{j+1}'s ring position (written out: a constexpr helper
+              // call here changes nvcc's unrolling of this loop at D=64 and
+              // costs 100 spill instructions)
+              int rk = 2 * (j + 1);
+              if constexpr (C::kConsumeOrder) rk = 2 * j + 1;
               mbar_wait_ctrl(smem_u32(&bars->s_read), uint32_t(j & 1));
               tc_fence_after();
               wait_full(rk);
               issue_qk(0, rk, C::s_col(j + 1));
               release(rk);
             }
-#ifndef TA_ROT_LATE
-            const int rv = 2 * j + 1;
+            int rv = 2 * j + 1;  // V_j
+            if constexpr (C::kConsumeOrder) rv = j + 1 < n ? 2 * j + 2 : 2 * n - 1;
             wait_full(rv);
             issue_pv(0, rv, j > 0, j);
             release(rv);
-#endif
           }
           umma_commit_warp(smem_u32(&bars->o_last));
         }
