@@ -175,6 +175,25 @@ def _stats_out(st: _Stats, stats: Optional[KernelStats]) -> None:
         setattr(stats, f, getattr(st, f))
 
 
+_DEFAULT_SCHEDULE = None
+
+
+def _default_schedule():
+    global _DEFAULT_SCHEDULE
+    if _DEFAULT_SCHEDULE is None:
+        _DEFAULT_SCHEDULE = TileSchedule()._c()
+    return _DEFAULT_SCHEDULE
+
+
+def _current_stream(device) -> int:
+    """Raw pointer of torch's current stream on ``device`` (fast path)."""
+    import torch
+    try:
+        return torch._C._cuda_getCurrentRawStream(device.index)
+    except (AttributeError, TypeError):
+        return torch.cuda.current_stream(device).cuda_stream
+
+
 def _mask_args(mask_kind: int, valid_len):
     if mask_kind == MASK_PADDING:
         if valid_len is None:
@@ -190,14 +209,15 @@ def sdpa_fwd(q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, lse_ptr: int, shape
              stream: int = 0, stats: Optional[KernelStats] = None) -> None:
     """Raw device-pointer entry (ta_sdpa_fwd)."""
     keep, vl = _mask_args(mask_kind, valid_len)
-    st = _Stats()
-    sched = (schedule or TileSchedule())._c()
+    st = _Stats() if stats is not None else None
+    sched = schedule._c() if schedule is not None else _default_schedule()
     rc = lib().ta_sdpa_fwd(q_ptr, k_ptr, v_ptr, o_ptr, lse_ptr or None, _Shape(*shape), dtype,
                            mask_kind, vl, 0 if scale is None else 1,
                            0.0 if scale is None else float(scale), sched, stream or None,
-                           ctypes.byref(st))
+                           ctypes.byref(st) if st is not None else None)
     _check(rc)
-    _stats_out(st, stats)
+    if st is not None:
+        _stats_out(st, stats)
 
 
 def sdpa_fwd_host(q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, lse_ptr: int,
@@ -252,12 +272,16 @@ def sdpa(q, k, v, causal: bool = False, scale: Optional[float] = None, *,
         lse = lse_out if lse_out is not None else torch.empty((B, H, S), device=q.device,
                                                               dtype=torch.float32)
     mask_kind = MASK_CAUSAL if causal else (MASK_PADDING if valid_len is not None else MASK_NONE)
-    stream = torch.cuda.current_stream(q.device).cuda_stream
-    with torch.cuda.device(q.device):
-        sdpa_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
-                 lse.data_ptr() if lse is not None else 0, (B, H, S, D), dt,
-                 mask_kind=mask_kind, valid_len=valid_len, scale=scale, schedule=schedule,
-                 stream=stream, stats=stats)
+    stream = _current_stream(q.device)
+    args = (q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+            lse.data_ptr() if lse is not None else 0, (B, H, S, D), dt)
+    kw = dict(mask_kind=mask_kind, valid_len=valid_len, scale=scale, schedule=schedule,
+              stream=stream, stats=stats)
+    if torch.cuda.current_device() == q.device.index:
+        sdpa_fwd(*args, **kw)
+    else:
+        with torch.cuda.device(q.device):
+            sdpa_fwd(*args, **kw)
     return (o, lse) if return_lse else o
 
 

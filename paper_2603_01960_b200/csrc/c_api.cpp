@@ -92,9 +92,6 @@ ta_status validate_device_support(ta_shape sh, ta_dtype dt, ta_mask_kind mask) {
   if (sh.d > 256 || sh.d % 8 != 0)
     return fail(TA_ERR_UNSUPPORTED, "head dim " + std::to_string(sh.d) +
                                         " not supported (D a multiple of 8, D <= 256)");
-  if (mask == TA_MASK_PADDING && sh.b > ta::kMaxPaddingBatch)
-    return fail(TA_ERR_UNSUPPORTED, "padding masks support B <= " +
-                                        std::to_string(ta::kMaxPaddingBatch));
   if (sh.s > (int64_t(1) << 30)) return fail(TA_ERR_UNSUPPORTED, "S too large");
   if (ta::fwd_geometry(sh.s, sh.b * sh.h, sh.d).ctas > 0x7FFFFFFF)
     return fail(TA_ERR_UNSUPPORTED, "more than 2^31 - 1 CTAs (B*H*ceil(S/rows per CTA))");
@@ -163,8 +160,8 @@ EncodeTiledFn encode_fn() {
 }
 
 // [BH][rows][cols] 16-bit tensor, boxes of 64 cols (128 B, SWIZZLE_128B) x box_rows.
-ta_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t bh, int64_t rows,
-                    int64_t cols, uint32_t box_rows) {
+ta_status encode_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t bh, int64_t rows,
+                      int64_t cols, uint32_t box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(rows), cuuint64_t(bh)};
@@ -177,6 +174,41 @@ ta_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t bh, int6
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return TA_OK;
+}
+
+// Per-thread memo of recent tensor maps (the same q/k/v buffers recur call
+// after call; a map is a pure function of these fields), so the small-shape
+// host path pays no encode.
+ta_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t bh, int64_t rows,
+                    int64_t cols, uint32_t box_rows) {
+  struct Entry {
+    const void* ptr = nullptr;
+    int64_t bh = 0, rows = 0, cols = 0;
+    uint32_t box_rows = 0;
+    bool bf16 = false;
+    CUtensorMap map;
+  };
+  constexpr int kEntries = 8;
+  thread_local Entry memo[kEntries];
+  thread_local int next = 0;
+  for (const Entry& e : memo)
+    if (e.ptr == ptr && e.ptr != nullptr && e.bh == bh && e.rows == rows && e.cols == cols &&
+        e.box_rows == box_rows && e.bf16 == bf16) {
+      *m = e.map;
+      return TA_OK;
+    }
+  ta_status st = encode_tmap(m, ptr, bf16, bh, rows, cols, box_rows);
+  if (st != TA_OK) return st;
+  Entry& e = memo[next];
+  next = (next + 1) % kEntries;
+  e.ptr = ptr;
+  e.bh = bh;
+  e.rows = rows;
+  e.cols = cols;
+  e.box_rows = box_rows;
+  e.bf16 = bf16;
+  e.map = *m;
   return TA_OK;
 }
 
@@ -274,9 +306,28 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.args.mask = int(mask_args.kind);
   L.args.heads = int(mask_args.heads);
   L.args.bh_offset = int(mask_args.bh_offset);
-  if (mask_args.kind == TA_MASK_PADDING)
-    for (int64_t b = 0; b < mask_args.batches; ++b)
-      L.args.valid_len[b] = int(mask_args.valid_len[b]);
+  // padding lengths: inline for B <= kInlinePadding, else a stream-ordered
+  // device array (allocated, filled and freed on the launch stream)
+  int* vl_dev = nullptr;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  if (mask_args.kind == TA_MASK_PADDING) {
+    if (mask_args.batches <= ta::kInlinePadding) {
+      for (int64_t b = 0; b < mask_args.batches; ++b)
+        L.args.valid_len[b] = int(mask_args.valid_len[b]);
+    } else {
+      std::vector<int> vl(size_t(mask_args.batches));
+      for (int64_t b = 0; b < mask_args.batches; ++b) vl[size_t(b)] = int(mask_args.valid_len[b]);
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&vl_dev), vl.size() * sizeof(int), cs);
+      if (e != cudaSuccess) return cuda_fail(e, "padding lengths (device array)");
+      // pageable source: returns once vl is staged, so the vector may go
+      e = cudaMemcpyAsync(vl_dev, vl.data(), vl.size() * sizeof(int), cudaMemcpyHostToDevice, cs);
+      if (e != cudaSuccess) {
+        cudaFreeAsync(vl_dev, cs);
+        return cuda_fail(e, "padding lengths (copy)");
+      }
+      L.args.valid_len_dev = vl_dev;
+    }
+  }
   L.bh = bh;
   L.head_dim = ta::fwd_kernel_head_dim(sh.d);  // kernel instantiation
   L.args.head_dim = int(sh.d);         // row length of q/k/v/o in memory
@@ -284,6 +335,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.stream = stream;
 
   cudaError_t e = ta::launch_sdpa_fwd(L);
+  if (vl_dev != nullptr) cudaFreeAsync(vl_dev, cs);  // after the kernel, stream-ordered
   if (e != cudaSuccess) return cuda_fail(e, "sdpa_fwd launch");
   return TA_OK;
 }

@@ -213,7 +213,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
   // bounds the K/V tiles a query tile visits (kv_end = last_row / t_n + 1,
   // tiled.cpp:159).  n_kv_t[t] is the trip count of Q tile t.
   const int kv_len =
-      args.mask == kMaskPadding ? args.valid_len[(args.bh_offset + bh) / args.heads] : S;
+      args.mask != kMaskPadding ? S
+      : args.valid_len_dev != nullptr ? args.valid_len_dev[(args.bh_offset + bh) / args.heads]
+                                      : args.valid_len[(args.bh_offset + bh) / args.heads];
   const int n_kv_seq = (kv_len + kBN - 1) / kBN;
   const int diag0 = q0 / kBN;  // K/V tile on Q tile 0's diagonal
   int n_kv_t[kQTiles] = {0, 0};

@@ -12,7 +12,10 @@ namespace ta {
 // MaskKind (reference types.hpp:41-76)
 enum FwdMask { kMaskNone = 0, kMaskCausal = 1, kMaskPadding = 2 };
 // key-side padding lengths travel in the kernel parameters (no device copy)
-constexpr int kMaxPaddingBatch = 1024;
+// padding lengths of up to kInlinePadding batches travel in the kernel
+// parameters; more come through a device array (a 4 KB parameter block
+// measured +3.5 us per launch)
+constexpr int kInlinePadding = 32;
 
 struct FwdArgs {
   void* o;           // [BH, S, D] 16-bit, same dtype as inputs
@@ -27,7 +30,8 @@ struct FwdArgs {
   // diagnostics: when non-null, CTA (0,0) records clock64 timestamps
   // trace[event * kTraceIters + j] for the first kTraceIters K/V iterations
   long long* trace;
-  int valid_len[kMaxPaddingBatch];  // Padding: keys j < valid_len[b] admitted
+  int valid_len[kInlinePadding];  // Padding: keys j < valid_len[b] admitted (B <= 32)
+  const int* valid_len_dev;       // ... or this device array [B] (nullptr: inline)
 };
 
 constexpr int kTraceIters = 64;

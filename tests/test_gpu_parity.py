@@ -358,6 +358,27 @@ def test_padding_matches_oracle(ta, cuda_device, dt, D):
     _check_lse(lse, r["lse"])
 
 
+def test_padding_many_batches_device_array(ta, cuda_device):
+    # B = 70 > 32 inline lengths: valid_len travels as a stream-ordered device
+    # array; every batch keeps its own length (incl. 0 and S)
+    import torch
+    B, H, S, D = 70, 2, 200, 64
+    g = torch.Generator(device="cuda").manual_seed(21)
+    q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=torch.bfloat16, generator=g)
+               for _ in range(3))
+    vl = [(b * 37) % (S + 1) for b in range(B)]
+    vl[5], vl[6] = 0, S
+    o = ta.sdpa(q, k, v, valid_len=vl)
+    for b in (0, 5, 6, 33, 69):
+        n = vl[b]
+        if n == 0:
+            assert not torch.any(o[b])
+            continue
+        ref = torch.nn.functional.scaled_dot_product_attention(
+            q[b].float(), k[b, :, :n].float(), v[b, :, :n].float())
+        assert (o[b].float() - ref).abs().max().item() <= TOL[O.BF16], b
+
+
 def test_causal_long_sampled_heads(ta, cuda_device):
     q, k, v = O.make_input((1, 3, 4096, 128), O.BF16, 8)
     o, lse = run_gpu(ta, q, k, v, O.BF16, causal=True)
@@ -421,3 +442,27 @@ def test_causal_host_entry_matches_device(ta, cuda_device):
     ta.sdpa_fwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), 0,
                      tuple(q.shape), ta.BF16, mask_kind=ta.MASK_CAUSAL)
     assert torch.equal(o, ta.sdpa(q.cuda(), k.cuda(), v.cuda(), causal=True).cpu())
+
+
+def test_tensor_map_memo_with_rotating_buffers(ta, cuda_device):
+    # the C-ABI memoises the last 8 tensor maps per thread: 12 distinct
+    # buffer sets of two shapes in rotation (evictions, pointer reuse after
+    # free) must each produce their own result
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(11)
+    sets = []
+    for i in range(12):
+        S = 256 if i % 2 else 384
+        sets.append([torch.randn(1, 2, S, 64, device="cuda", dtype=torch.bfloat16, generator=g)
+                     for _ in range(3)])
+    refs = [torch.nn.functional.scaled_dot_product_attention(*(x.float() for x in s)) for s in sets]
+    for _ in range(3):
+        for s, r in zip(sets, refs):
+            assert (ta.sdpa(*s).float() - r).abs().max().item() <= TOL[O.BF16]
+    # free and reallocate: same addresses may come back with other contents
+    del sets
+    torch.cuda.empty_cache()
+    x = [torch.randn(1, 2, 256, 64, device="cuda", dtype=torch.bfloat16, generator=g)
+         for _ in range(3)]
+    r = torch.nn.functional.scaled_dot_product_attention(*(t.float() for t in x))
+    assert (ta.sdpa(*x).float() - r).abs().max().item() <= TOL[O.BF16]
