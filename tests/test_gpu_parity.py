@@ -139,7 +139,7 @@ def test_running_max_jumps_in_later_halves(ta, cuda_device, dt):
     # later K/V tile: drives every branch of the lazy rescale (the stale-max
     # slow path for half 0 and half 1 at both head dims; at D=64 under the
     # S/P rotation, where PV(j-1) may still be in flight) against the oracle.
-    for D in (64, 128):
+    for D in (64, 128, 256):
         q, k, v = O.make_input((1, 4, 512, D), dt, 91)
         q = np.full_like(q, 0.5)          # every row = 0.5 * ones (on the 16-bit grid)
         k = k * np.float32(0.125)         # exact power-of-2 scaling keeps k on the grid
@@ -344,7 +344,7 @@ def test_causal_matches_oracle(ta, cuda_device, dt, D, S):
 
 
 @pytest.mark.parametrize("dt", [O.F16, O.BF16])
-@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("D", [64, 128, 160, 256])
 def test_padding_matches_oracle(ta, cuda_device, dt, D):
     # test_tiled.cpp:359-370 + oracle empty rows: valid_len 0, ragged, full
     B, H, S = 4, 2, 300
