@@ -107,10 +107,6 @@ constexpr int kPParts = TA_P_PARTS;
 #endif
 constexpr bool kStaleMax = TA_STALE_MAX != 0;
 constexpr float kSumGuard = 256.0f;
-// MMA issue: 4 K-steps per elect (1) or one elect per K-step (0)
-#ifndef TA_MMA_BATCH
-#define TA_MMA_BATCH 1
-#endif
 
 #ifndef TA_SLOTS_D128
 #define TA_SLOTS_D128 4
@@ -341,6 +337,13 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
     {
       constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
       constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+      // wide kernels with a smaller head dim (D=160 on the 192-column kernel,
+      // TMA zero-fill past D): QK^T skips the all-zero K-steps and PV computes
+      // only the O columns that are stored (+4% at D=160; at D <= 128 the
+      // loop is softmax-bound and the trimming measured -1%, so it is off)
+      const int n_kstep = D > 128 ? (args.head_dim + 15) >> 4 : D / 16;
+      const uint32_t idesc_pv_n =
+          D > 128 ? (idesc_pv & ~(0x3Fu << 17)) | (uint32_t(n_kstep * 16 >> 3) << 17) : idesc_pv;
       // ring position r (K_j at 2j, V_j at 2j+1) -> slot / phase
       auto slot_of = [](int r) { return r % C::kSlots; };
       auto phase_of = [](int r) { return uint32_t((r / C::kSlots) & 1); };
@@ -357,20 +360,17 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
       auto issue_qk = [&](int t, int r, uint32_t scol = 0) {
         uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
         uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
-#if TA_MMA_BATCH
+        const uint32_t dS = tmem + C::kTmemS + t * kBN + scol;
 #pragma unroll
         for (int r = 0; r < C::kRegions; ++r) {  // 4 K-steps of 16 per 128-B swizzle region
           const uint32_t off = (r * C::kRegionBytes) >> 4;
-          umma_ss_x4<2, 2>(tmem + C::kTmemS + t * kBN + scol, qd + off, kd + off, idesc_qk, r > 0);
+          if (D <= 128 || n_kstep >= 4 * r + 4) {
+            umma_ss_x4<2, 2>(dS, qd + off, kd + off, idesc_qk, r > 0);
+          } else {  // head dim below the kernel's: skip the all-zero K-steps
+            for (int ks = 0; ks < n_kstep - 4 * r; ++ks)
+              umma_ss_warp(dS, qd + off + 2 * ks, kd + off + 2 * ks, idesc_qk, (r > 0 || ks > 0));
+          }
         }
-#else
-        asm volatile("" : "+l"(qd), "+l"(kd));
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = ((ks >> 2) * C::kRegionBytes + (ks & 3) * 32) >> 4;
-          umma_ss_warp(tmem + C::kTmemS + t * kBN + scol, qd + off, kd + off, idesc_qk, ks > 0);
-        }
-#endif
         umma_commit_warp(smem_u32(&bars->s_full[t]));
       };
       // PV in two halves of 64 keys, each issued as soon as the softmax
@@ -385,26 +385,14 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
           if (h == kPParts - 1 && lane == 0) rec(t == 0 ? kEvMmaWaitP0 : kEvMmaWaitP1, j);
           static_assert((kBN / 16 / kPParts) % 4 == 0, "P part = 4k K-steps of 16 keys");
           constexpr int kSteps = kBN / 16 / kPParts;
-#if TA_MMA_BATCH
 #pragma unroll
           for (int g = 0; g < kSteps / 4; ++g) {
             const int ks0 = h * kSteps + g * 4;
             constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
             umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tP + ks0 * 8,
-                               vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv,
+                               vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv_n,
                                (accumulate || ks0 > 0) ? 1u : 0u);
           }
-#else
-          const int ks0 = h * 4;
-          asm volatile("" : "+l"(vd));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int ks = ks0 + kk;
-            umma_ts_warp(tmem + C::kTmemO + t * D, tP + ks * 8,
-                         vd + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
-                         (accumulate || ks > 0) ? 1u : 0u);
-          }
-#endif
           if (kStale && h == 0) umma_commit_warp(smem_u32(&bars->o_half[t]));
         }
         umma_commit_warp(smem_u32(&bars->o_full[t]));
