@@ -26,7 +26,7 @@ for j in range(n):
 import numpy as np
 print(f"kernel start {t[21, 0] - base}, after setup {t[21, 1] - base}, "
       f"epilogue done tile0 {t[22, 0] - base} tile1 {t[22, 1] - base}, "
-      f"last P arrive tile1 {t[13, min(n, 64) - 1] - base}")
+      f"last P arrive tile0 {t[8, min(n, 64) - 1] - base} tile1 {t[13, min(n, 64) - 1] - base}")
 js = range(8, n - 1)
 def d(a, b): return np.mean([t[b, j] - t[a, j] for j in js])
 print("mean over iters 8..n-2 (cycles):")
