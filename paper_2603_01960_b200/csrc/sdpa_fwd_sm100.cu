@@ -225,7 +225,33 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
   };
 
   if (threadIdx.x == 0) rec(kEvKernelStart, 0);
-  if (threadIdx.x == kWarpMma * 32) {
+  // ring position p -> K (kv = 0) or V (kv = 1) of tile j: K_j, V_j
+  // alternating, or (kConsumeOrder) the rotation's consumption order K_0,
+  // K_1, V_0, K_2, V_1, ..., K_{n-1}, V_{n-2}, V_{n-1}
+  auto ring_tile = [&](int p, int& kv, int& j) {
+    if constexpr (!C::kConsumeOrder) {
+      kv = p & 1;
+      j = p >> 1;
+    } else {
+      kv = p == 0 ? 0 : p == 2 * n_kv - 1 ? 1 : (p & 1) ? 0 : 1;
+      j = p == 0 ? 0 : p == 2 * n_kv - 1 ? n_kv - 1 : (p & 1) ? (p + 1) >> 1 : (p - 2) >> 1;
+    }
+  };
+  auto load_ring = [&](int p) {
+    int kv, j;
+    ring_tile(p, kv, j);
+    const int slot = p % C::kSlots;
+    const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+    mbar_arrive_expect_tx(fbar, C::kTileBytes);
+    for (int r = 0; r < C::kRegions; ++r)
+      tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, kv == 0 ? &tmap_k : &tmap_v,
+                  fbar, r * 64, j * kBN, bh);
+  };
+  // The TMA thread initialises the barriers and issues Q and the first ring
+  // fill before the CTA barrier (fresh slots need no empty-wait), so the
+  // loads overlap the TMEM allocation and the barrier round trip.
+  const int ring_prefill = min(C::kSlots, 2 * n_kv);
+  if (threadIdx.x == R::kWarpTma * 32) {
     mbar_init(smem_u32(&bars->q_full), 1);
     for (int t = 0; t < kQTiles; ++t)
       for (int q = 0; q < kPParts; ++q)
@@ -242,6 +268,16 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
       mbar_init(smem_u32(&bars->slot_empty[s]), 1);
     }
     fence_barrier_init();
+    tma_prefetch_desc(&tmap_q);
+    tma_prefetch_desc(&tmap_k);
+    tma_prefetch_desc(&tmap_v);
+    const uint32_t qbar = smem_u32(&bars->q_full);
+    if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQT * C::kTileBytes);
+    for (int t = 0; t < kQT && n_kv > 0; ++t)  // (no key admitted: Q unused)
+      for (int r = 0; r < C::kRegions; ++r)
+        tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
+                    q0 + t * kBM, bh);
+    for (int p = 0; p < ring_prefill; ++p) load_ring(p);
   }
   if (warp == kWarpAlloc) tmem_alloc<R::kTmemCols>(smem_u32(&bars->tmem_base));
   tc_fence_before();
@@ -256,60 +292,10 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
   if (warp == kWarpTma) {
     // ------------------------------------------------------------------ TMA
     if (lane == 0) {
-      tma_prefetch_desc(&tmap_q);
-      tma_prefetch_desc(&tmap_k);
-      tma_prefetch_desc(&tmap_v);
-      const uint32_t qbar = smem_u32(&bars->q_full);
-      if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQT * C::kTileBytes);
-      for (int t = 0; t < kQT && n_kv > 0; ++t)  // (no key admitted: Q unused)
-        for (int r = 0; r < C::kRegions; ++r)
-          tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
-                      q0 + t * kBM, bh);
-#if TA_KV_EVICT_LAST
-      const uint64_t kv_policy = l2_policy_evict_last();  // K/V re-read by the head's CTAs
-#endif
-      int slot = 0;
-      uint32_t phase = 0;
-      if constexpr (!C::kConsumeOrder) {
-        // ring positions: K_j at 2j, V_j at 2j+1
-        for (int j = 0; j < n_kv; ++j) {
-          for (int kv = 0; kv < 2; ++kv) {
-            mbar_wait_ctrl(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
-            const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-            mbar_arrive_expect_tx(fbar, C::kTileBytes);
-            const CUtensorMap* map = kv == 0 ? &tmap_k : &tmap_v;
-            for (int r = 0; r < C::kRegions; ++r)
-#if TA_KV_EVICT_LAST
-              tma_load_3d_hint(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar,
-                               r * 64, j * kBN, bh, kv_policy);
-#else
-              tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
-                          j * kBN, bh);
-#endif
-            if (++slot == C::kSlots) {
-              slot = 0;
-              phase ^= 1;
-            }
-          }
-        }
-      } else {
-        // the order the rotation consumes them: K_0, K_1, V_0, K_2, V_1, ...,
-        // K_{n-1}, V_{n-2}, V_{n-1} (position p -> tile)
-        for (int p = 0; p < 2 * n_kv; ++p) {
-          const bool is_k = p == 0 || (p != 2 * n_kv - 1 && (p & 1));
-          const int j = p == 0 ? 0 : p == 2 * n_kv - 1 ? n_kv - 1 : (p & 1) ? (p + 1) >> 1 : (p - 2) >> 1;
-          mbar_wait_ctrl(smem_u32(&bars->slot_empty[slot]), phase ^ 1);
-          const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-          mbar_arrive_expect_tx(fbar, C::kTileBytes);
-          const CUtensorMap* map = is_k ? &tmap_k : &tmap_v;
-          for (int r = 0; r < C::kRegions; ++r)
-            tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, map, fbar, r * 64,
-                        j * kBN, bh);
-          if (++slot == C::kSlots) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
+      for (int p = ring_prefill; p < 2 * n_kv; ++p) {
+        mbar_wait_ctrl(smem_u32(&bars->slot_empty[p % C::kSlots]),
+                       uint32_t((p / C::kSlots) & 1) ^ 1u);
+        load_ring(p);
       }
     }
   } else if (warp == kWarpTrace) {
