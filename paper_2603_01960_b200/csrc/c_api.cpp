@@ -294,10 +294,13 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   const uint32_t kv_rows = uint32_t(plan.block_n);  // one TMA box = one K/V tile row block
   if ((st = make_tmap(&mk, k, bf16, bh, sh.s, sh.d, kv_rows)) != TA_OK) return st;
   if ((st = make_tmap(&mv, v, bf16, bh, sh.s, sh.d, kv_rows)) != TA_OK) return st;
+  CUtensorMap mo;
+  if ((st = make_tmap(&mo, o, bf16, bh, sh.s, sh.d, 128)) != TA_OK) return st;
   ta::FwdLaunch L{};
   L.tmap_q = &mq;
   L.tmap_k = &mk;
   L.tmap_v = &mv;
+  L.tmap_o = &mo;
   L.args.o = o;
   L.args.lse = lse;
   L.args.seq_len = int(sh.s);

@@ -114,6 +114,10 @@ constexpr float kSumGuard = 256.0f;
 #ifndef TA_TRACE_ROW  // row whose softmax phases the diagnostic trace records
 #define TA_TRACE_ROW 0
 #endif
+#ifndef TA_TMA_STORE_O  // epilogue: TMA store of O from shared memory (1) or 16-B global stores (0)
+#define TA_TMA_STORE_O 1
+#endif
+constexpr bool kTmaStoreO = TA_TMA_STORE_O != 0;
 #ifndef TA_SLOTS_D64
 #define TA_SLOTS_D64 4
 #endif
@@ -175,7 +179,8 @@ template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>>
 __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::kMinBlocks)
     sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
-                    const __grid_constant__ CUtensorMap tmap_v, FwdArgs args) {
+                    const __grid_constant__ CUtensorMap tmap_v,
+                    const __grid_constant__ CUtensorMap tmap_o, FwdArgs args) {
   using C = Cfg<D, kQT>;
   using R = RolesFor<D, kQT>;
   constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
@@ -694,6 +699,10 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
     const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
     const int dm = args.head_dim;  // stored columns (<= D)
     uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * dm;
+    // TMA-store epilogue: the tile's rows go to its (now dead) Q buffer in the
+    // 128B-swizzled layout the O tensor map expects, then one thread stores
+    // the tile (rows >= S and columns >= D clipped by the map)
+    const uint32_t so = sq + t * C::kTileBytes;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t orow[32];
@@ -710,7 +719,14 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
       for (int i = 0; i < 16; ++i)
         packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
                                  __uint_as_float(orow[2 * i + 1]) * inv_l);
-      if (grow < S) {
+      if constexpr (kTmaStoreO) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // 16-B chunk k of the row's 128-B line, XOR row % 8
+          const uint32_t k = uint32_t((c & 1) * 4 + i);
+          st_shared_v4(so + (c >> 1) * C::kRegionBytes + row * 128 + ((k ^ (row & 7)) << 4),
+                       packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+        }
+      } else if (grow < S) {
         uint4* dst = reinterpret_cast<uint4*>(orow_g + c * 32);
 #pragma unroll
         for (int i = 0; i < 4; ++i)  // 16-B pieces of 8 columns; dm is a multiple of 8
@@ -719,9 +735,19 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
                                 packed[4 * i + 3]);
       }
     }
+    if constexpr (kTmaStoreO) {
+      fence_proxy_async_smem();
+      named_bar_sync(1 + t, kBM);  // the tile's four softmax warps
+      if (row == 0) {
+        for (int r = 0; r < C::kRegions; ++r)
+          if (r * 64 < dm) tma_store_3d(&tmap_o, so + r * C::kRegionBytes, r * 64, q0 + t * kBM, bh);
+        tma_store_commit();
+      }
+    }
     if (args.lse != nullptr && grow < S)
       args.lse[size_t(bh) * S + grow] =
           l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+    if (kTmaStoreO && row == 0) tma_store_wait_read0();  // smem stays valid until read
     if (kTrace && row == 0) rec(kEvEpilogueDone, t);
   }
 
@@ -840,7 +866,7 @@ cudaError_t launch_typed(const FwdLaunch& L) {
   if (ctas > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned int>(ctas), 1u, 1u);
   kern<<<grid, RolesFor<D, kQT>::kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
-      *L.tmap_q, *L.tmap_k, *L.tmap_v, L.args);
+      *L.tmap_q, *L.tmap_k, *L.tmap_v, *L.tmap_o, L.args);
   return cudaGetLastError();
 }
 

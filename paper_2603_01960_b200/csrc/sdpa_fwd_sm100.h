@@ -67,6 +67,7 @@ struct FwdLaunch {
   const CUtensorMap* tmap_q;
   const CUtensorMap* tmap_k;
   const CUtensorMap* tmap_v;
+  const CUtensorMap* tmap_o;  // O, boxes of 64 cols x 128 rows (epilogue TMA store)
   FwdArgs args;
   int64_t bh;
   int head_dim;  // kernel instantiation: 64 or 128
