@@ -466,3 +466,23 @@ def test_tensor_map_memo_with_rotating_buffers(ta, cuda_device):
          for _ in range(3)]
     r = torch.nn.functional.scaled_dot_product_attention(*(t.float() for t in x))
     assert (ta.sdpa(*x).float() - r).abs().max().item() <= TOL[O.BF16]
+
+
+@pytest.mark.parametrize("D", [64, 96, 128, 160, 256])
+def test_tiny_and_ragged_sequences_all_kernels(ta, cuda_device, D):
+    # S = 1 (one query, one key), S < one tile, S one past a tile, on every
+    # kernel instantiation, both masks, with LSE
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(31 + D)
+    for S in (1, 17, 129):
+        q, k, v = (torch.randn(2, 3, S, D, device="cuda", dtype=torch.float16, generator=g)
+                   for _ in range(3))
+        for causal in (False, True):
+            o, lse = ta.sdpa(q, k, v, causal=causal, return_lse=True)
+            s = (q.float() @ k.float().transpose(-1, -2)) / math.sqrt(D)
+            if causal:
+                s = s.masked_fill(torch.ones(S, S, device="cuda", dtype=torch.bool).triu(1),
+                                  float("-inf"))
+            ref = torch.softmax(s, -1) @ v.float()
+            assert (o.float() - ref).abs().max().item() <= TOL[O.F16], (S, causal)
+            assert (lse - torch.logsumexp(s, -1)).abs().max().item() <= LSE_TOL, (S, causal)
