@@ -141,7 +141,7 @@ static void test_tiled_kernel_matches_the_reference_oracle() {  // test_tiled.cp
   PlanCache cache;
   for (int64_t s : {32, 130}) {
     for (DType dt : {DType::F16Emu, DType::BF16Emu}) {
-      for (int64_t d : {64, 96, 128}) {
+      for (int64_t d : {64, 96, 128, 160, 256}) {
         const AttnInput in = make_input(Shape{1, 2, s, d}, dt, 77);
         for (const MaskSpec& mask : {MaskSpec::none(), MaskSpec::causal(),
                                      MaskSpec::padding({std::max<int64_t>(1, s / 2)})}) {
