@@ -6,18 +6,23 @@
 Workload (BASELINE.json configs[4], the config the metric's 1/2/4/8-GPU
 scaling is quoted on and the largest that fits one GPU):
     long-context B=8 H=64 S=32768 D=128 bf16, non-causal, default scale.
-A "step" is one forward over the whole tensor.  At N GPUs each rank owns H/N
-heads for every batch (head sharding) — no collective on the
-data path; total work is fixed, so scaling is "strong".
+A "step" is one forward (O and LSE) over the whole tensor.  At N GPUs each
+rank owns H/N heads for every batch (head sharding) — no
+collective on the data path; total work is fixed, so scaling is "strong".
+`--gpus N` under torchrun uses its environment; without a launcher bench.py
+starts the N ranks itself (one process per GPU, 127.0.0.1 rendezvous).
 
 Metric: TFLOP/s = 4*B*H*S^2*D / t (reference analysis.cpp:25-30), t the max
-over ranks of the CUDA-event time of the K timed steps.  Inputs (2.1 GB) are
-far larger than L2 (126 MB), so no flush is needed between steps.
+over ranks of the CUDA-event time of the K timed steps; per-step median and
+nearest-rank p95 as the reference harness reports them (bench.cpp:19-33).
+Inputs (3 x 4.3 GB) are far larger than L2 (126 MB), so no flush is needed
+between steps.
 
 `--impl reference` times the reference's own CPU implementation
 (tileattn::sdpa_tiled compiled from its sources into oracle/_ref) on the
 host cores: each step is a bounded sample of the same workload — one full
-(b,h) head, S=32768, D=128 (1/512 of the job).
+(b,h) head, S=32768, D=128 (1/512 of the job), the same bytes as the GPU
+arm's first head.
 """
 from __future__ import annotations
 
@@ -109,148 +114,280 @@ class ClockSampler:
                 "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------ CPU baseline
-def cpu_reference_rate(S=32768, D=128, schedules=((64, 128, 2, 0), (128, 128, 2, 1)),
-                       runs=1):
-    """Reference tileattn::sdpa_tiled (oracle/_ref) on one (b,h) head of the
-    workload, all host threads.  Returns (TFLOP/s of the faster schedule, info)."""
-    import oracle
-    R = oracle.ref("auto")
-    q, k, v = oracle.make_input((1, 1, S, D), oracle.BF16, 0)
-    h = R.ref_handle_new(q.ravel().copy(), k.ravel().copy(), v.ravel().copy(), 1, 1, S, D,
-                         oracle.BF16)
-    best = None
+# ------------------------------------------------------------ inputs
+SEED = 1234
+
+
+def sample_head(S, D, seed=SEED):
+    """(q, k, v) of head (b=0, h=0) of rank 0's input, generated on the host
+    (torch CPU generator, N(0,1) snapped to bf16): the GPU arm uploads these
+    exact bytes as its first head and both CPU arms (cpu_baseline and
+    --impl reference) time the reference on them (identical bytes)."""
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    return tuple(torch.randn(S, D, generator=g).to(torch.bfloat16) for _ in range(3))
+
+
+def cpu_model():
     try:
-        for (tm, tn, st, lay) in schedules:
-            ts = []
-            for _ in range(runs):
-                t0 = time.perf_counter()
-                rc = R.ref_handle_run(h, tm, tn, st, lay, 0, None)
-                ts.append(time.perf_counter() - t0)
-                if rc != 0:
-                    raise RuntimeError(R.ref_last_error())
-            t = min(ts)
-            if best is None or t < best[0]:
-                best = (t, (tm, tn, st, "col" if lay else "row"))
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def quantiles(samples):
+    """Median and nearest-rank p95 exactly as the reference harness
+    (bench.cpp:19-33): p95 = sorted[ceil(0.95 n) - 1] in integer arithmetic."""
+    xs = sorted(samples)
+    n = len(xs)
+    med = xs[n // 2] if n % 2 else 0.5 * (xs[n // 2 - 1] + xs[n // 2])
+    return med, xs[(19 * n + 19) // 20 - 1]
+
+
+# ------------------------------------------------------------ CPU baseline
+SCHEDULES = {"row": (64, 128, 2, 0),   # reference default TileSchedule{} (tiled.hpp:30-37)
+             "col": (128, 128, 2, 1)}  # the reference's faster layout on this path
+
+
+class _RefHead:
+    """The reference tileattn::sdpa_tiled (oracle/_ref) on one (b,h) head."""
+
+    def __init__(self, S, D):
+        import numpy as np
+        import oracle
+        self.S, self.D = S, D
+        self.R = oracle.ref("auto")
+        self.lib_name = oracle.ref_variant("auto").name
+        q, k, v = (np.ascontiguousarray(x.float().numpy()).ravel() for x in sample_head(S, D))
+        self.h = self.R.ref_handle_new(q, k, v, 1, 1, S, D, oracle.BF16)
+
+    def run(self, sched):
+        if self.R.ref_handle_run(self.h, *sched, 0, None) != 0:
+            raise RuntimeError(self.R.ref_last_error())
+
+    def time(self, sched, steps, warmup):
+        for _ in range(warmup):
+            self.run(sched)
+        ts = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            self.run(sched)
+            ts.append(time.perf_counter() - t0)
+        return ts
+
+    def close(self):
+        self.R.ref_handle_free(self.h)
+
+
+def cpu_reference_rate(S=32768, D=128):
+    """cpu_baseline leg: both reference schedules on one head of the workload,
+    all host threads, one run each.  Returns (TF/s of the faster, info)."""
+    ref = _RefHead(S, D)
+    try:
+        secs = {name: ref.time(sc, 1, 0)[0] for name, sc in SCHEDULES.items()}
     finally:
-        R.ref_handle_free(h)
-    rate = flops(1, 1, S, D) / best[0] / 1e12
-    return rate, dict(seconds=best[0], schedule=list(best[1]),
-                      lib=oracle.ref_variant("auto").name)
+        ref.close()
+    best = min(secs, key=secs.get)
+    rates = {n: flops(1, 1, S, D) / t / 1e12 for n, t in secs.items()}
+    return rates[best], dict(seconds=secs, rates=rates, best=best, lib=ref.lib_name)
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0  # N>1: rank 0 alone runs the CPU reference
-    import oracle
-    S, D = WORKLOAD["S"], WORKLOAD["D"]
-    R = oracle.ref("auto")
-    q, k, v = oracle.make_input((1, 1, S, D), oracle.BF16, 0)
-    h = R.ref_handle_new(q.ravel().copy(), k.ravel().copy(), v.ravel().copy(), 1, 1, S, D,
-                         oracle.BF16)
-    sched = (64, 128, 2, 0)  # reference default TileSchedule{} (tiled.hpp:30-37)
-    if args.ref_schedule == "col":
-        sched = (128, 128, 2, 1)
+    S, D = args.cpu_sample_s, WORKLOAD["D"]
+    ref = _RefHead(S, D)
     try:
-        for _ in range(args.warmup):
-            R.ref_handle_run(h, *sched, 0, None)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            if R.ref_handle_run(h, *sched, 0, None) != 0:
-                raise RuntimeError(R.ref_last_error())
-        dt = time.perf_counter() - t0
+        # value: the faster reference schedule (col) over K steps; the
+        # default schedule (row) is timed beside it over min(K, 2) steps
+        ts = {"col": ref.time(SCHEDULES["col"], args.steps, args.warmup),
+              "row": ref.time(SCHEDULES["row"], min(args.steps, 2), min(args.warmup, 1))}
     finally:
-        R.ref_handle_free(h)
-    ms = dt / args.steps * 1e3
-    val = flops(1, 1, S, D) / (dt / args.steps) / 1e12
+        ref.close()
+    per = {n: flops(1, 1, S, D) / (sum(t) / len(t)) / 1e12 for n, t in ts.items()}
+    ms = sum(ts["col"]) / len(ts["col"]) * 1e3
+    val = per["col"]
     cores = os.cpu_count()
+    med, p95 = quantiles([t * 1e3 for t in ts["col"]])
+    sample = (f"one (b,h) head of the workload per step (S={S}, D={D}; "
+              f"{'1/512 of the job' if S == 32768 else 'reduced S'}), bytes identical to the "
+              f"GPU arm's head 0; schedule {{128,128,2,col}} (the faster; default "
+              f"{{64,128,2,row}} measured {per['row']:.4f} TF/s), {ref.lib_name}")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "ms_per_step_median": med, "ms_per_step_p95": p95,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic N(0,1) snapped to the bf16 grid (reference make_input, seed 0)",
+        "data": "synthetic N(0,1) snapped to bf16 (torch CPU generator, seed 1234)",
         "config": dict(WORKLOAD, parallelism="cpu threads"),
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"one (b,h) head of the workload per step (S={S}, D={D}; "
-                                   f"1/512 of the job), schedule t_m={sched[0]} t_n={sched[1]} "
-                                   f"stages={sched[2]} {'col' if sched[3] else 'row'}, "
-                                   f"{oracle.ref_variant('auto').name}"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(),
+                         "kind": "reference", "sample": sample,
+                         "schedules": {"col": per["col"], "row": per["row"]}},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------ launch
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` with no launcher: start N local ranks (one
+    process per GPU, the torchrun environment), rank 0's stdout is the
+    output; other ranks' stdout goes to stderr."""
+    port = _free_port()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()),
+                                       *sys.argv[1:]], env=env,
+                                      stdout=None if r == 0 else sys.stderr))
+    rcs = [p.wait() for p in procs]
+    return max(rcs)
+
+
 # ------------------------------------------------------------------ our arm
+class _EventClock:
+    """CUDA events on the launching stream (device time)."""
+
+    def __init__(self, stream):
+        import torch
+        self.torch, self.stream = torch, stream
+
+    def mark(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def ms(self, a, b):
+        return a.elapsed_time(b)
+
+
+class _HostClock:
+    """--stub-step (CPU orchestration test): host wall clock."""
+
+    def mark(self):
+        return time.perf_counter()
+
+    def ms(self, a, b):
+        return (b - a) * 1e3
+
+
+def timed_steps(step, clock, steps, warmup, barrier):
+    """W untimed steps, then exactly K timed steps bracketed by barrier +
+    synchronize on both sides; one mark pair per step.  Returns (total ms of
+    the K steps on this rank, per-step ms)."""
+    for _ in range(warmup):
+        step()
+    barrier()
+    marks = []
+    t_start = clock.mark()
+    for _ in range(steps):
+        a = clock.mark()
+        step()
+        marks.append((a, clock.mark()))
+    t_end = clock.mark()
+    barrier()
+    return clock.ms(t_start, t_end), [clock.ms(a, b) for a, b in marks]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    import paper_2603_01960_b200 as ta
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    stub = args.stub_step
+    if stub:
+        dev = torch.device("cpu")
+        if world > 1:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        if world > 1:
+            # NCCL communicator lines (nranks) in the log; nothing on the
+            # data path uses it (barriers and the max-over-ranks timing only)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2603_01960_b200.sharding import head_range, max_over_ranks
     B, H, S, D = WORKLOAD["B"], WORKLOAD["H"], WORKLOAD["S"], WORKLOAD["D"]
     h0, h1 = head_range(H, world, rank)  # head sharding: this rank owns heads [h0, h1)
     Hl = h1 - h0
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q, k, v = (torch.randn(B, Hl, S, D, device=dev, generator=g, dtype=torch.bfloat16)
-               for _ in range(3))
-    o = torch.empty_like(q)
-    stream = torch.cuda.current_stream(dev)
-    stats = ta.KernelStats()
-
-    def step():
-        ta.sdpa(q, k, v, out=o, stats=stats)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
-        torch.cuda.synchronize(dev)
+        if not stub:
+            torch.cuda.synchronize(dev)
 
-    # ---- device-timed region: K steps, one event pair per step on the
-    # launching stream (kernel launch duration = step duration here)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    barrier()
-    with ClockSampler(local) as clk:
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        for e0, e1 in evs:
-            e0.record(stream)
-            step()
-            e1.record(stream)
-        t_end.record(stream)
-        barrier()
-    total_ms = t_start.elapsed_time(t_end)
-    per_launch = [e0.elapsed_time(e1) for e0, e1 in evs]
+    stats = None
+    if stub:
+        # orchestration test only: a fixed CPU step stands in for the kernel
+        a = torch.randn(192, 192)
+        step = lambda: a @ a  # noqa: E731
+        clock = _HostClock()
+        job_flops = flops(B, H, S, D)
+    else:
+        import paper_2603_01960_b200 as ta
+        g = torch.Generator(device=dev).manual_seed(SEED + rank)
+        q, k, v = (torch.randn(B, Hl, S, D, device=dev, generator=g, dtype=torch.bfloat16)
+                   for _ in range(3))
+        if rank == 0:  # head 0: the bytes the CPU arms time (sample_head)
+            for x, hx in zip((q, k, v), sample_head(S, D)):
+                x[0, 0].copy_(hx)
+        o = torch.empty_like(q)
+        lse = torch.empty((B, Hl, S), device=dev, dtype=torch.float32)
+        stream = torch.cuda.current_stream(dev)
+        stats = ta.KernelStats()
+
+        def step():
+            ta.sdpa(q, k, v, out=o, return_lse=True, lse_out=lse, stats=stats)
+
+        clock = _EventClock(stream)
+        job_flops = flops(B, H, S, D)
+
+    sampler = ClockSampler(local) if not stub else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        total_ms, per_step = timed_steps(step, clock, args.steps, args.warmup, barrier)
+    finally:
+        if sampler:
+            sampler.__exit__(None, None, None)
     if world > 1:
         total_ms = max_over_ranks(total_ms, device=dev)
+        per_step = [max_over_ranks(x, device=dev) for x in per_step]
     ms_step = total_ms / args.steps
-    job_flops = flops(B, H, S, D)
     value = job_flops / (ms_step / 1e3) / 1e12
+    med, p95 = quantiles(per_step)
 
     # ---- roofline of the dominant (only) kernel, per launch
     pk, pk_kind = peaks()
-    launch_ms = statistics.mean(per_launch)
+    launch_ms = statistics.mean(per_step)
     achieved = flops(B, Hl, S, D) / (launch_ms / 1e3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
+    if prof.exists() and not stub:
         try:
             ps = json.loads(prof.read_text())
             if ps.get("workload") == WORKLOAD["workload"] and world == 1:
@@ -259,22 +396,24 @@ def run_ours(args):
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"],
                 "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"], "traffic": traffic,
+                "traffic_source": "profiles/ncu_summary.json (ncu --set full of this workload)",
                 "peak_kind": f"{pk_kind} burst bf16 (MEASURED_PEAKS.json bf16_tflops)",
                 "frac_of_sustained": achieved / pk.get("bf16_tflops_sustained",
                                                        pk["bf16_tflops"]),
                 "algorithmic_bytes_per_launch": 8 * B * Hl * S * D + 4 * B * Hl * S}
 
     # ---- e2e through the public host-buffer entry (ta_sdpa_fwd_host):
-    # pinned host q/k/v -> H2D, kernel, D2H of O, every step
+    # pinned host q/k/v -> H2D, kernel, D2H of O and LSE, every step
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not stub:
         hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
         ho = torch.empty_like(hq).pin_memory()
+        hl = torch.empty((B, Hl, S), dtype=torch.float32).pin_memory()
         shape = (B, Hl, S, D)
-        ptrs = (hq.data_ptr(), hk.data_ptr(), hv.data_ptr(), ho.data_ptr())
+        ptrs = (hq.data_ptr(), hk.data_ptr(), hv.data_ptr(), ho.data_ptr(), hl.data_ptr())
 
         def e2e_step():
-            ta.sdpa_fwd_host(*ptrs, 0, shape, ta.BF16, stream=stream.cuda_stream)
+            ta.sdpa_fwd_host(*ptrs, shape, ta.BF16, stream=stream.cuda_stream)
 
         e2e_step()
         barrier()
@@ -286,21 +425,28 @@ def run_ours(args):
         e2e_s = (time.perf_counter() - t0) / n_e2e
         if world > 1:
             e2e_s = max_over_ranks(e2e_s, device=dev)
-        nbytes = q.numel() * 2
+        nbytes = B * H * S * D * 2
         e2e = {"value": job_flops / e2e_s / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": 3 * nbytes * world, "d2h_bytes_per_step": nbytes * world,
+               "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes + 4 * B * H * S,
                "ms_per_step": e2e_s * 1e3, "steps": n_e2e,
-               "path": "ta_sdpa_fwd_host (C-ABI, pinned host buffers, includes copies)"}
-        del hq, hk, hv, ho
+               "path": "ta_sdpa_fwd_host (C-ABI, pinned host buffers, includes copies of "
+                       "q/k/v in and O/LSE out)"}
+        del hq, hk, hv, ho, hl
 
+    # ---- CPU baseline: rank 0, every N (bounded sample, after the timed
+    # region; the other ranks wait at the final barrier)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            rate, info = cpu_reference_rate()
-            cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"one (b,h) head of the workload (S=32768, D=128; 1/512 of the "
-                             f"job), best of schedules {{64,128,2,row}}/{{128,128,2,col}} -> "
-                             f"{info['schedule']}, {info['seconds']:.2f} s, {info['lib']}"}
+            rate, info = cpu_reference_rate(S=args.cpu_sample_s, D=D)
+            cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(),
+                   "cpu_model": cpu_model(), "kind": "reference",
+                   "sample": f"one (b,h) head of the workload (S={args.cpu_sample_s}, D={D}; "
+                             f"bytes identical to the GPU arm's head 0), schedules "
+                             f"{{64,128,2,row}} {info['rates']['row']:.4f} / "
+                             f"{{128,128,2,col}} {info['rates']['col']:.4f} TF/s -> best "
+                             f"{info['best']}, {info['lib']}",
+                   "schedules": info["rates"]}
         except Exception as exc:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -309,21 +455,26 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "ms_per_step_median": med, "ms_per_step_p95": p95,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16",
-            "data": "synthetic N(0,1) bf16 (torch.randn on device, seed 1234+rank)",
+            "data": "synthetic N(0,1) bf16 (torch.randn on device, seed 1234+rank; head 0 of "
+                    "rank 0 = the CPU arms' sample head)",
             "config": dict(WORKLOAD, parallelism=f"head-shard{world}", heads_per_gpu=Hl,
-                           l2="inputs 2.1 GB >> 126 MB L2; no flush needed"),
+                           l2="inputs 3 x 4.3 GB >> 126 MB L2; no flush needed"),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "clocks": clk.summary(),
-            "gpu_launches": args.steps,
-            "kernel": {"name": "ta::sdpa_fwd_kernel<128,bf16>", "ctas": stats.ctas,
-                       "block_m": stats.block_m, "block_n": stats.block_n,
-                       "stages": stats.stages, "q_tiles_per_cta": stats.q_tiles_per_cta,
-                       "per_launch_ms": [round(x, 4) for x in per_launch]},
+            "clocks": sampler.summary() if sampler else None,
+            "gpu_launches": 0 if stub else args.steps,
         }
+        if stub:
+            line["stub"] = "orchestration test: CPU step, gloo, host clock (not a measurement)"
+        else:
+            line["kernel"] = {"name": "ta::sdpa_fwd_kernel<128,bf16>", "ctas": stats.ctas,
+                              "block_m": stats.block_m, "block_n": stats.block_n,
+                              "stages": stats.stages, "q_tiles_per_cta": stats.q_tiles_per_cta,
+                              "per_launch_ms": [round(x, 4) for x in per_step]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -399,7 +550,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--ref-schedule", choices=["row", "col"], default="row")
+    ap.add_argument("--cpu-sample-s", type=int, default=WORKLOAD["S"],
+                    help="S of the CPU arms' one-head sample (default: the workload's)")
+    ap.add_argument("--stub-step", action="store_true",
+                    help="CPU orchestration test (gloo, stub step); not a measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="all BASELINE configs (report only)")
@@ -410,6 +564,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.sweep:
+        return spawn_ranks(args)
     if args.sweep:
         return run_sweep(args)
     return run_ours(args)

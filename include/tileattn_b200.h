@@ -95,7 +95,10 @@ typedef struct ta_kernel_stats {
  *             tiled.hpp:223-238, tiled.cpp:216-220)
  *   lse     : device, [B,H,S] fp32 natural-log log-sum-exp of the scaled
  *             scores (m + ln l); -inf for rows with no admitted key; NULL = skip
- *   valid_len : HOST array of B entries, MaskKind::Padding only (else NULL)
+ *   valid_len : HOST array of B entries, MaskKind::Padding only (else NULL);
+ *             B <= 32 travels in the kernel parameters, larger B through a
+ *             per-device pool of pinned/device slots (allocated on first
+ *             use, reused once the launch that read a slot has completed)
  *   has_scale/scale : ScaleSpec (types.hpp:78-86); has_scale = 0 -> 1/sqrt(D)
  *   stats   : optional out-parameter (KernelStats analogue), may be NULL
  *
@@ -108,13 +111,20 @@ TA_API ta_status ta_sdpa_fwd(const void* q, const void* k, const void* v, void* 
                       ta_schedule sched, void* stream, ta_kernel_stats* stats);
 
 /* Host-buffer entry (the end-to-end path): q/k/v/o/lse are HOST pointers
- * (pinned for full PCIe bandwidth; pageable works).  Copies in, runs the
- * device entry, copies O (and LSE) back, and synchronises `stream`.  Device
- * workspace is cached per device and grown on demand. */
+ * (pinned for full PCIe bandwidth and for the chunked H2D / compute / D2H
+ * overlap; pageable works, but each pageable copy blocks the host, which
+ * serialises the pipeline).  Copies in, runs the device entry, copies O (and
+ * LSE) back, and synchronises `stream`; on an error part-way every stream is
+ * drained before returning.  Device workspace (4 tensors + LSE) is cached
+ * per device and grown on demand; ta_release_workspace frees it. */
 TA_API ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o, float* lse,
                            ta_shape shape, ta_dtype dtype, ta_mask_kind mask,
                            const int64_t* valid_len, int has_scale, double scale,
                            ta_schedule sched, void* stream, ta_kernel_stats* stats);
+
+/* Free the per-device workspace of ta_sdpa_fwd_host and the padding-length
+ * pool (after draining their streams).  The next call re-allocates. */
+TA_API ta_status ta_release_workspace(int device);
 
 /* Validation only: the status ta_sdpa_fwd / ta_sdpa_fwd_host would return for
  * these arguments before touching any device (reference order shape -> mask ->
@@ -152,6 +162,14 @@ TA_API int ta_device_supported(int device);
  * a, b: device 16-bit; d: device fp32 [128][128].  Synchronous. */
 TA_API ta_status ta_debug_umma_gemm(int mode, ta_dtype dtype, const void* a, const void* b, float* d,
                              void* stream);
+
+/* Diagnostics: y[i] = 2^x[i] on the device with the softmax's exp2 units
+ *   mode 0: ex2_poly2, the FMA-pipe emulation (tiled.hpp:94-118 fast_expf
+ *           construction in base 2: round-to-nearest split, degree-3
+ *           polynomial, exponent insertion by integer add)
+ *   mode 1: MUFU ex2.approx.ftz
+ * x, y: device fp32 [n].  Synchronous. */
+TA_API ta_status ta_debug_exp2(const float* x, float* y, int64_t n, int mode, void* stream);
 
 /* Diagnostics: run the forward once with a cycle-timeline trace of CTA (0,0):
  * trace (device, int64[24 * 64]) receives clock64 stamps per event and K/V

@@ -9,7 +9,7 @@
 // snapped to the dtype grid (tiled.cpp:216-220); std::invalid_argument for bad
 // shapes / masks / scales, UnsupportedScheduleError for bad schedules and for
 // what the sm_100a kernel does not cover (F32 / F64 accumulation, D not a
-// multiple of 8 or above 128).  Header-only: include it and link
+// multiple of 8 or above 256).  Header-only: include it and link
 // libtileattn_b200.so.
 #pragma once
 

@@ -25,7 +25,7 @@ from typing import Optional, Sequence
 __all__ = [
     "TileSchedule", "KernelStats", "UnsupportedScheduleError", "CudaError", "lib",
     "sdpa", "sdpa_fwd", "sdpa_fwd_host", "sdpa_tiled", "schedule_supported",
-    "effective_scale", "plan_cache_stats", "plan_cache_clear", "F32", "F16", "BF16",
+    "effective_scale", "plan_cache_stats", "plan_cache_clear", "release_workspace", "F32", "F16", "BF16",
     "MASK_NONE", "MASK_CAUSAL", "MASK_PADDING",
 ]
 
@@ -126,6 +126,10 @@ def lib() -> ctypes.CDLL:
     L.ta_device_supported.argtypes = [cint]
     L.ta_sdpa_check.restype = cint
     L.ta_sdpa_check.argtypes = [_Shape, cint, cint, vp, cint, dbl, _Schedule]
+    L.ta_release_workspace.restype = cint
+    L.ta_release_workspace.argtypes = [cint]
+    L.ta_debug_exp2.restype = cint
+    L.ta_debug_exp2.argtypes = [vp, vp, i64, cint, vp]
     L.ta_debug_umma_gemm.restype = cint
     L.ta_debug_umma_gemm.argtypes = [cint, cint, vp, vp, vp, vp]
     _lib = L
@@ -167,6 +171,11 @@ def plan_cache_clear() -> None:
     lib().ta_plan_cache_clear()
 
 
+def release_workspace(device: int = 0) -> None:
+    """Free the host-entry workspace and padding pool of ``device``."""
+    _check(lib().ta_release_workspace(int(device)))
+
+
 def _stats_out(st: _Stats, stats: Optional[KernelStats]) -> None:
     if stats is None:
         return
@@ -194,9 +203,13 @@ def _current_stream(device) -> int:
         return torch.cuda.current_stream(device).cuda_stream
 
 
-def _mask_args(mask_kind: int, valid_len):
+def _mask_args(mask_kind: int, valid_len, shape):
     if mask_kind == MASK_PADDING:
-        if valid_len is None:
+        # the C-ABI reads valid_len[0..B-1]: a shorter list would be read past
+        # its end (the reference validates the size, types.cpp:99-106).  A bad
+        # shape is left to the library, which reports it first (shape -> mask).
+        shape_ok = all(int(x) >= 1 for x in shape)
+        if valid_len is None or (shape_ok and len(valid_len) != int(shape[0])):
             raise ValueError("padding mask needs one valid_len per batch")
         arr = (ctypes.c_int64 * len(valid_len))(*[int(x) for x in valid_len])
         return arr, ctypes.cast(arr, ctypes.c_void_p)
@@ -208,7 +221,7 @@ def sdpa_fwd(q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, lse_ptr: int, shape
              scale: Optional[float] = None, schedule: Optional[TileSchedule] = None,
              stream: int = 0, stats: Optional[KernelStats] = None) -> None:
     """Raw device-pointer entry (ta_sdpa_fwd)."""
-    keep, vl = _mask_args(mask_kind, valid_len)
+    keep, vl = _mask_args(mask_kind, valid_len, shape)
     st = _Stats() if stats is not None else None
     sched = schedule._c() if schedule is not None else _default_schedule()
     rc = lib().ta_sdpa_fwd(q_ptr, k_ptr, v_ptr, o_ptr, lse_ptr or None, _Shape(*shape), dtype,
@@ -226,7 +239,7 @@ def sdpa_fwd_host(q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, lse_ptr: int,
                   schedule: Optional[TileSchedule] = None, stream: int = 0,
                   stats: Optional[KernelStats] = None) -> None:
     """Raw host-pointer entry (ta_sdpa_fwd_host): H2D, kernel, D2H, sync."""
-    keep, vl = _mask_args(mask_kind, valid_len)
+    keep, vl = _mask_args(mask_kind, valid_len, shape)
     st = _Stats()
     sched = (schedule or TileSchedule())._c()
     rc = lib().ta_sdpa_fwd_host(q_ptr, k_ptr, v_ptr, o_ptr, lse_ptr or None, _Shape(*shape),
@@ -261,14 +274,26 @@ def sdpa(q, k, v, causal: bool = False, scale: Optional[float] = None, *,
         raise ValueError("q, k, v must share one [B,H,S,D] shape")
     if not (q.is_cuda and k.is_cuda and v.is_cuda):
         raise ValueError("q, k, v must be CUDA tensors (no CPU fallback)")
+    if k.device != q.device or v.device != q.device:
+        raise ValueError("q, k, v must be on one device")
     if q.dtype != k.dtype or q.dtype != v.dtype:
         raise ValueError("q, k, v must share one dtype")
     dt = _torch_dtype_code(q)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     B, H, S, D = q.shape
+    # caller buffers are written through raw pointers as a contiguous
+    # [B,H,S,D] 16-bit O and a contiguous [B,H,S] fp32 LSE: check exactly that
+    if out is not None and (out.shape != q.shape or out.dtype != q.dtype
+                            or out.device != q.device or not out.is_contiguous()):
+        raise ValueError("out must be a contiguous tensor of q's shape, dtype and device")
     o = out if out is not None else torch.empty_like(q)
     lse = None
     if return_lse:
+        if lse_out is not None and (tuple(lse_out.shape) != (B, H, S)
+                                    or lse_out.dtype != torch.float32
+                                    or lse_out.device != q.device
+                                    or not lse_out.is_contiguous()):
+            raise ValueError("lse_out must be a contiguous float32 [B,H,S] tensor on q's device")
         lse = lse_out if lse_out is not None else torch.empty((B, H, S), device=q.device,
                                                               dtype=torch.float32)
     mask_kind = MASK_CAUSAL if causal else (MASK_PADDING if valid_len is not None else MASK_NONE)

@@ -72,7 +72,9 @@ ta_status validate_common(ta_shape sh, ta_mask_kind mask, const int64_t* valid_l
                                         " stages=" + std::to_string(sched.stages));
   // scale (types.cpp:108-116)
   if (has_scale) {
-    if (!(scale > 0.0))
+    // the reference predicate (types.cpp:108-116 throws for *scale <= 0.0):
+    // NaN passes, as there, and propagates into O / LSE
+    if (scale <= 0.0)
       return fail(TA_ERR_INVALID_ARGUMENT, "effective_scale: explicit scale must be > 0");
     *eff_scale = scale;
   } else {
@@ -275,6 +277,80 @@ void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh, ta_mask_kind ma
   st->reserved = 0;
 }
 
+// Device copies of padding lengths for B > kInlinePadding: a per-device pool
+// of (pinned host, device, event) slots.  A slot is taken when its last
+// launch has completed (event query), so steady-state calls allocate nothing
+// and the copy source is pinned (asynchronous).
+struct PaddingSlot {
+  int* host = nullptr;
+  int* dev = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  bool busy = false;
+};
+
+struct PaddingPool {
+  std::mutex mu;
+  std::vector<std::unique_ptr<PaddingSlot>> slots;
+};
+
+PaddingPool& padding_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<PaddingPool>> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& p = pools[dev];
+  if (!p) p = std::make_unique<PaddingPool>();
+  return *p;
+}
+
+void release_padding_pool(int dev) {
+  PaddingPool& pool = padding_pool(dev);
+  std::lock_guard<std::mutex> lock(pool.mu);
+  for (auto& sl : pool.slots) {
+    if (sl->done) cudaEventSynchronize(sl->done);
+    if (sl->dev) cudaFree(sl->dev);
+    if (sl->host) cudaFreeHost(sl->host);
+    if (sl->done) cudaEventDestroy(sl->done);
+  }
+  pool.slots.clear();
+}
+
+ta_status padding_slot(size_t n, PaddingSlot** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  PaddingPool& pool = padding_pool(dev);
+  std::lock_guard<std::mutex> lock(pool.mu);
+  PaddingSlot* pick = nullptr;
+  for (auto& sl : pool.slots) {
+    if (sl->busy || sl->cap < n) continue;
+    const cudaError_t q = cudaEventQuery(sl->done);
+    if (q == cudaSuccess) {
+      pick = sl.get();
+      break;
+    }
+    if (q != cudaErrorNotReady) return cuda_fail(q, "padding slot event");
+  }
+  if (pick == nullptr) {
+    auto sl = std::make_unique<PaddingSlot>();
+    const size_t cap = std::max<size_t>(n, 1024);
+    cudaError_t e;
+    if ((e = cudaMallocHost(reinterpret_cast<void**>(&sl->host), cap * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(reinterpret_cast<void**>(&sl->dev), cap * sizeof(int))) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming)) != cudaSuccess) {
+      if (sl->host) cudaFreeHost(sl->host);
+      if (sl->dev) cudaFree(sl->dev);
+      cudaGetLastError();
+      return cuda_fail(e, "padding lengths (pool slot)");
+    }
+    sl->cap = cap;
+    pick = sl.get();
+    pool.slots.push_back(std::move(sl));
+  }
+  pick->busy = true;
+  *out = pick;
+  return TA_OK;
+}
+
 struct MaskArgs {
   ta_mask_kind kind = TA_MASK_NONE;
   const int64_t* valid_len = nullptr;  // host, [B] (padding)
@@ -309,26 +385,26 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.args.mask = int(mask_args.kind);
   L.args.heads = int(mask_args.heads);
   L.args.bh_offset = int(mask_args.bh_offset);
-  // padding lengths: inline for B <= kInlinePadding, else a stream-ordered
-  // device array (allocated, filled and freed on the launch stream)
-  int* vl_dev = nullptr;
+  // padding lengths: inline for B <= kInlinePadding, else a device array
+  // from the per-device pool (pinned staging, stream-ordered copy; a slot is
+  // reused once the launch that read it has completed)
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  PaddingSlot* slot = nullptr;
   if (mask_args.kind == TA_MASK_PADDING) {
     if (mask_args.batches <= ta::kInlinePadding) {
       for (int64_t b = 0; b < mask_args.batches; ++b)
         L.args.valid_len[b] = int(mask_args.valid_len[b]);
     } else {
-      std::vector<int> vl(size_t(mask_args.batches));
-      for (int64_t b = 0; b < mask_args.batches; ++b) vl[size_t(b)] = int(mask_args.valid_len[b]);
-      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&vl_dev), vl.size() * sizeof(int), cs);
-      if (e != cudaSuccess) return cuda_fail(e, "padding lengths (device array)");
-      // pageable source: returns once vl is staged, so the vector may go
-      e = cudaMemcpyAsync(vl_dev, vl.data(), vl.size() * sizeof(int), cudaMemcpyHostToDevice, cs);
+      ta_status pst = padding_slot(size_t(mask_args.batches), &slot);
+      if (pst != TA_OK) return pst;
+      for (int64_t b = 0; b < mask_args.batches; ++b) slot->host[b] = int(mask_args.valid_len[b]);
+      cudaError_t e = cudaMemcpyAsync(slot->dev, slot->host, size_t(mask_args.batches) * sizeof(int),
+                                      cudaMemcpyHostToDevice, cs);
       if (e != cudaSuccess) {
-        cudaFreeAsync(vl_dev, cs);
+        slot->busy = false;
         return cuda_fail(e, "padding lengths (copy)");
       }
-      L.args.valid_len_dev = vl_dev;
+      L.args.valid_len_dev = slot->dev;
     }
   }
   L.bh = bh;
@@ -338,7 +414,12 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.stream = stream;
 
   cudaError_t e = ta::launch_sdpa_fwd(L);
-  if (vl_dev != nullptr) cudaFreeAsync(vl_dev, cs);  // after the kernel, stream-ordered
+  if (slot != nullptr) {
+    // the slot is free again once this launch (which read it) completes
+    cudaError_t er = cudaEventRecord(slot->done, cs);
+    slot->busy = false;
+    if (e == cudaSuccess && er != cudaSuccess) e = er;
+  }
   if (e != cudaSuccess) return cuda_fail(e, "sdpa_fwd launch");
   return TA_OK;
 }
@@ -391,7 +472,7 @@ int ta_schedule_supported(ta_schedule sched) { return schedule_ok(sched) ? 1 : 0
 ta_status ta_effective_scale(int has_scale, double scale, int64_t d, double* out) {
   if (d < 1) return fail(TA_ERR_INVALID_ARGUMENT, "effective_scale: D must be >= 1");
   if (has_scale) {
-    if (!(scale > 0.0))
+    if (scale <= 0.0)  // reference predicate: NaN is accepted (types.cpp:108-116)
       return fail(TA_ERR_INVALID_ARGUMENT, "effective_scale: explicit scale must be > 0");
     if (out) *out = scale;
     return TA_OK;
@@ -498,47 +579,90 @@ ta_status ta_sdpa_fwd_host(const void* q, const void* k, const void* v, void* o,
                                ? std::min<int64_t>({bh, int64_t(Workspace::kMaxChunks), max_chunks})
                                : 1);
   if ((st = ws.ensure_streams()) != TA_OK) return st;
-  int64_t h0 = 0;
-  for (int c = 0; c < n_chunks; ++c) {
-    const int64_t h1 = bh * (c + 1) / n_chunks;
-    const int64_t hc = h1 - h0;
-    if (hc == 0) continue;
-    const size_t off = size_t(h0) * head_elems * 2, bytes = size_t(hc) * head_elems * 2;
-    // inputs of this chunk, ordered after the previous call's use of the
-    // workspace (the compute stream's last event)
-    if ((e = cudaStreamWaitEvent(ws.h2d, ws.ev_compute_done, 0)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dq + off, static_cast<const char*>(q) + off, bytes,
-                             cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dk + off, static_cast<const char*>(k) + off, bytes,
-                             cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dv + off, static_cast<const char*>(v) + off, bytes,
-                             cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
-        (e = cudaEventRecord(ws.ev_in[c], ws.h2d)) != cudaSuccess ||
-        (e = cudaStreamWaitEvent(s, ws.ev_in[c], 0)) != cudaSuccess)
-      return cuda_fail(e, "H2D copy");
-    const ta_shape cs{1, hc, shape.s, shape.d};
-    MaskArgs mk{mask, valid_len, shape.h, h0, shape.b};
-    if ((st = run_device(dq + off, dk + off, dv + off, dout + off,
-                         dl ? dl + size_t(h0) * size_t(shape.s) : nullptr, cs, dtype, eff, *plan,
-                         stream, mk)) != TA_OK)
-      return st;
-    if ((e = cudaEventRecord(ws.ev_out[c], s)) != cudaSuccess ||
-        (e = cudaStreamWaitEvent(ws.d2h, ws.ev_out[c], 0)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(static_cast<char*>(o) + off, dout + off, bytes,
-                             cudaMemcpyDeviceToHost, ws.d2h)) != cudaSuccess)
-      return cuda_fail(e, "D2H copy");
-    if (lse &&
-        (e = cudaMemcpyAsync(lse + size_t(h0) * size_t(shape.s), dl + size_t(h0) * size_t(shape.s),
-                             size_t(hc) * size_t(shape.s) * 4, cudaMemcpyDeviceToHost,
-                             ws.d2h)) != cudaSuccess)
-      return cuda_fail(e, "D2H copy");
-    h0 = h1;
+  // enqueue the whole pipeline; on a failure part-way, drain every stream
+  // before returning so no copy still reads the caller's q/k/v or writes o
+  // (and the next call cannot reuse the workspace under them)
+  auto enqueue = [&]() -> ta_status {
+    int64_t h0 = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int64_t h1 = bh * (c + 1) / n_chunks;
+      const int64_t hc = h1 - h0;
+      if (hc == 0) continue;
+      const size_t off = size_t(h0) * head_elems * 2, bytes = size_t(hc) * head_elems * 2;
+      // inputs of this chunk, ordered after the previous call's use of the
+      // workspace (the compute stream's last event)
+      if ((e = cudaStreamWaitEvent(ws.h2d, ws.ev_compute_done, 0)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(dq + off, static_cast<const char*>(q) + off, bytes,
+                               cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(dk + off, static_cast<const char*>(k) + off, bytes,
+                               cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(dv + off, static_cast<const char*>(v) + off, bytes,
+                               cudaMemcpyHostToDevice, ws.h2d)) != cudaSuccess ||
+          (e = cudaEventRecord(ws.ev_in[c], ws.h2d)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(s, ws.ev_in[c], 0)) != cudaSuccess)
+        return cuda_fail(e, "H2D copy");
+      const ta_shape cs{1, hc, shape.s, shape.d};
+      MaskArgs mk{mask, valid_len, shape.h, h0, shape.b};
+      ta_status rst = run_device(dq + off, dk + off, dv + off, dout + off,
+                                 dl ? dl + size_t(h0) * size_t(shape.s) : nullptr, cs, dtype, eff,
+                                 *plan, stream, mk);
+      if (rst != TA_OK) return rst;
+      if ((e = cudaEventRecord(ws.ev_out[c], s)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(ws.d2h, ws.ev_out[c], 0)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(static_cast<char*>(o) + off, dout + off, bytes,
+                               cudaMemcpyDeviceToHost, ws.d2h)) != cudaSuccess)
+        return cuda_fail(e, "D2H copy");
+      if (lse && (e = cudaMemcpyAsync(lse + size_t(h0) * size_t(shape.s),
+                                      dl + size_t(h0) * size_t(shape.s),
+                                      size_t(hc) * size_t(shape.s) * 4, cudaMemcpyDeviceToHost,
+                                      ws.d2h)) != cudaSuccess)
+        return cuda_fail(e, "D2H copy");
+      h0 = h1;
+    }
+    return TA_OK;
+  };
+  st = enqueue();
+  if (st != TA_OK) {
+    const std::string msg = g_last_error;
+    cudaStreamSynchronize(ws.h2d);
+    cudaStreamSynchronize(ws.d2h);
+    cudaStreamSynchronize(s);
+    cudaEventRecord(ws.ev_compute_done, s);
+    g_last_error = msg;
+    return st;
   }
   if ((e = cudaEventRecord(ws.ev_compute_done, s)) != cudaSuccess)
     return cuda_fail(e, "event record");
   if ((e = cudaStreamSynchronize(ws.d2h)) != cudaSuccess) return cuda_fail(e, "D2H sync");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
   fill_stats(stats, *plan, shape, mask, valid_len);
+  return TA_OK;
+}
+
+ta_status ta_release_workspace(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "release workspace");
+  }
+  if (device < 0 || device >= n) return fail(TA_ERR_INVALID_ARGUMENT, "no such device");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "release workspace");
+  {
+    Workspace& ws = workspace(device);
+    std::lock_guard<std::mutex> lock(ws.mu);
+    if (ws.h2d) cudaStreamSynchronize(ws.h2d);
+    if (ws.d2h) cudaStreamSynchronize(ws.d2h);
+    if (ws.ev_compute_done) cudaEventSynchronize(ws.ev_compute_done);
+    if (ws.ptr) e = cudaFree(ws.ptr);
+    ws.ptr = nullptr;
+    ws.bytes = 0;
+  }
+  release_padding_pool(device);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(e, "release workspace");
   return TA_OK;
 }
 
@@ -556,6 +680,18 @@ ta_status ta_debug_sdpa_trace(const void* q, const void* k, const void* v, void*
     return st;
   cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "trace sync");
+  return TA_OK;
+}
+
+ta_status ta_debug_exp2(const float* x, float* y, int64_t n, int mode, void* stream) {
+  if (mode < 0 || mode > 1) return fail(TA_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+  if (n < 0 || (n > 0 && (!x || !y))) return fail(TA_ERR_INVALID_ARGUMENT, "x, y, n");
+  ta_status st;
+  if ((st = check_device()) != TA_OK) return st;
+  cudaError_t e = ta::launch_exp2_unit(x, y, n, mode, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "exp2 unit launch");
+  if ((e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream))) != cudaSuccess)
+    return cuda_fail(e, "exp2 unit sync");
   return TA_OK;
 }
 

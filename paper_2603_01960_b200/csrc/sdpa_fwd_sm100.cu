@@ -845,6 +845,24 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) tmem_dealloc<256>(tmem);
 }
 
+// exp2 unit under test: mode 0 = ex2_poly2 (the FMA-pipe emulation the
+// softmax uses for part of the columns), mode 1 = MUFU ex2.approx.ftz
+__global__ void exp2_unit_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n,
+                                 int mode) {
+  const int64_t i = 2 * (int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+  if (i >= n) return;
+  const float a = x[i], b = i + 1 < n ? x[i + 1] : 0.f;
+  float p0, p1;
+  if (mode == 0) {
+    ex2_poly2(f2(a, b), p0, p1);
+  } else {
+    p0 = ex2(a);
+    p1 = ex2(b);
+  }
+  y[i] = p0;
+  if (i + 1 < n) y[i + 1] = p1;
+}
+
 template <int D, bool kBF16>
 cudaError_t launch_typed(const FwdLaunch& L) {
   constexpr int kQT = kQTilesFor<D>;
@@ -896,6 +914,14 @@ cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
   if (L.head_dim == 192) return L.bf16 ? launch_typed<192, true>(L) : launch_typed<192, false>(L);
   if (L.head_dim == 256) return L.bf16 ? launch_typed<256, true>(L) : launch_typed<256, false>(L);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_exp2_unit(const float* x, float* y, int64_t n, int mode, void* stream) {
+  const int64_t pairs = (n + 1) / 2;
+  const unsigned blocks = unsigned((pairs + 255) / 256);
+  if (blocks > 0)
+    exp2_unit_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, y, n, mode);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_umma_selftest(const CUtensorMap* ta_map, const CUtensorMap* tb_map,

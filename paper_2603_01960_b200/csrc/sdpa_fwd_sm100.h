@@ -70,7 +70,7 @@ struct FwdLaunch {
   const CUtensorMap* tmap_o;  // O, boxes of 64 cols x 128 rows (epilogue TMA store)
   FwdArgs args;
   int64_t bh;
-  int head_dim;  // kernel instantiation: 64 or 128
+  int head_dim;  // kernel instantiation: 64, 128, 192 or 256
   bool bf16;
   void* stream;
 };
@@ -89,6 +89,7 @@ int fwd_ring_slots(int D);
 // the TMA boxes zero-fill the extra columns)
 int fwd_kernel_head_dim(int64_t D);
 cudaError_t launch_sdpa_fwd(const FwdLaunch& launch);
+cudaError_t launch_exp2_unit(const float* x, float* y, int64_t n, int mode, void* stream);
 cudaError_t launch_umma_selftest(const CUtensorMap* a_map, const CUtensorMap* b_map,
                                  const void* a_glob, float* d_out, int mode, bool bf16,
                                  void* stream);

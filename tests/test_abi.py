@@ -95,6 +95,36 @@ def test_validation_order_and_error_classes():
         _call(shape=(1, 1, 64, 264))
 
 
+def test_padding_length_must_match_batch():
+    # a short valid_len list would be read past its end by the C-ABI
+    with pytest.raises(ValueError, match="one valid_len per batch"):
+        _call(shape=(3, 1, 64, 64), mask_kind=ta.MASK_PADDING, valid_len=[64, 64])
+    with pytest.raises(ValueError, match="one valid_len per batch"):
+        _call(shape=(1, 1, 64, 64), mask_kind=ta.MASK_PADDING, valid_len=[64, 64])
+    # shape errors still come first (shape -> mask)
+    with pytest.raises(ValueError, match="shape"):
+        _call(shape=(0, 1, 64, 64), mask_kind=ta.MASK_PADDING, valid_len=[64, 64])
+
+
+def test_scale_predicate_matches_reference():
+    # types.cpp:108-116 throws only for *scale <= 0.0: NaN is accepted there
+    # and propagates into the output; the C-ABI follows the same predicate
+    import math
+    assert math.isnan(ta.effective_scale(64, float("nan")))
+    for bad in (0.0, -0.0, -1.0, float("-inf")):
+        with pytest.raises(ValueError, match="scale"):
+            ta.effective_scale(64, bad)
+    assert ta.effective_scale(64, float("inf")) == float("inf")
+
+
+def test_release_workspace_validates_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("host has a GPU")
+    with pytest.raises((ta.CudaError, ValueError)):
+        ta.release_workspace(0)
+
+
 def test_no_cpu_fallback_without_device():
     import torch
     if torch.cuda.is_available():

@@ -1,0 +1,165 @@
+"""GPU parity at every BASELINE.json config, at the real shapes.
+
+VERDICT r1 "missing #1": the kernel must match the CPU reference on every
+config `north_star` names, including the bench workload itself (B8 H64 S32K
+D128 bf16: 256 K/V tiles per row).  Each test runs the kernel over the whole
+config tensor on the GPU and checks sampled heads (first, middle and last
+flattened (b, h)) against
+
+  * O: the reference's own ``sdpa_tiled`` with ``AccumMode::F64``
+    (tiled.hpp:244; the mode the reference pins its fast path with,
+    test_tiled.cpp:293-303), compiled from the reference sources into
+    oracle/_ref (dtype F32 on the grid-valued input, so the oracle output is
+    not snapped: tiled.cpp:216-220);
+  * LSE: a row-blocked float64 restatement (oracle.sdpa_numpy's math, pinned
+    to the C oracle and the reference primitives in tests/test_oracle.py).
+
+Inputs are unit-variance normals snapped to the config's 16-bit grid
+(torch.randn on the device; the bytes of the sampled heads are what the
+reference receives).  Tolerances (max-abs on O): BASELINE north_star bf16
+2e-2 / f16 1e-2, and the reference's stricter f16 gate 5e-3 (bench.cpp:56-63);
+LSE 1e-3.  With TA_PARITY_OUT set, each sampled head's errors are appended
+there as JSON lines (collected into profiles/r02/parity.json).
+"""
+import json
+import math
+import os
+import time
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+O_TOL = {O.F16: 5e-3, O.BF16: 2e-2}
+LSE_TOL = 1e-3
+
+# BASELINE.json configs (name, (B, H, S, D), dtype)
+CONFIGS = [
+    ("cfg4_long_B8H64S32K_D128_bf16", (8, 64, 32768, 128), O.BF16),
+    ("cfg2_ssweep_S1K", (4, 16, 1024, 64), O.BF16),
+    ("cfg2_ssweep_S2K", (4, 16, 2048, 64), O.BF16),
+    ("cfg2_ssweep_S4K", (4, 16, 4096, 64), O.BF16),
+    ("cfg2_ssweep_S8K", (4, 16, 8192, 64), O.BF16),
+    ("cfg2_ssweep_S16K", (4, 16, 16384, 64), O.BF16),
+    ("cfg3_dsweep_D64_f16", (8, 32, 4096, 64), O.F16),
+    ("cfg3_dsweep_D64_bf16", (8, 32, 4096, 64), O.BF16),
+    ("cfg3_dsweep_D128_f16", (8, 32, 4096, 128), O.F16),
+    ("cfg3_dsweep_D128_bf16", (8, 32, 4096, 128), O.BF16),
+    ("cfg5_vit_B64H16S1K_D64_bf16", (64, 16, 1024, 64), O.BF16),
+]
+
+
+def _record(**fields):
+    path = os.environ.get("TA_PARITY_OUT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(fields) + "\n")
+
+
+def _ref_o_f64(q, k, v):
+    """reference sdpa_tiled, AccumMode::F64, one head [S, D] (f32 grid values)."""
+    R = O.ref("v4" if O._cpu_has_avx512() and O.ref_available("v4") else "exact")
+    S, D = q.shape
+    out = np.empty(S * D, np.float32)
+    # {128,128,2,col}: the reference's faster layout; schedule-invariant
+    # output within its own tolerance, F64 accumulation
+    rc = R.ref_sdpa_tiled(np.ascontiguousarray(q), np.ascontiguousarray(k),
+                          np.ascontiguousarray(v), 1, 1, S, D, O.F32, 0, 0.0, O.MASK_NONE, None,
+                          128, 128, 2, 1, 0, 1, out, None)
+    assert rc == 0, R.ref_last_error()
+    return out.reshape(S, D).astype(np.float64)
+
+
+def _lse_f64(q, k, scale, block=2048):
+    """Row-blocked float64 LSE of one head (sdpa_numpy's math)."""
+    q = q.astype(np.float64)
+    kt = k.astype(np.float64).T
+    out = np.empty(q.shape[0])
+    for r0 in range(0, q.shape[0], block):
+        s = (q[r0:r0 + block] @ kt) * scale
+        m = s.max(axis=1, keepdims=True)
+        out[r0:r0 + block] = m[:, 0] + np.log(np.exp(s - m).sum(axis=1))
+    return out
+
+
+@pytest.mark.parametrize("name,shape,dt", CONFIGS, ids=[c[0] for c in CONFIGS])
+def test_baseline_config_sampled_heads_vs_reference_f64(ta, cuda_device, name, shape, dt):
+    import torch
+    B, H, S, D = shape
+    tdt = torch.bfloat16 if dt == O.BF16 else torch.float16
+    g = torch.Generator(device="cuda").manual_seed(zlib.crc32(name.encode()))
+    q, k, v = (torch.randn(shape, device="cuda", generator=g).to(tdt) for _ in range(3))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    o, lse = ta.sdpa(q, k, v, return_lse=True)
+    torch.cuda.synchronize()
+    gpu_s = time.perf_counter() - t0
+    scale = 1.0 / math.sqrt(D)
+    BH = B * H
+    worst_o = worst_l = 0.0
+    for bh in sorted({0, BH // 2, BH - 1}):
+        b, h = divmod(bh, H)
+        qh, kh, vh = (x[b, h].float().cpu().numpy() for x in (q, k, v))
+        t1 = time.perf_counter()
+        ro = _ref_o_f64(qh, kh, vh)
+        rl = _lse_f64(qh, kh, scale)
+        ref_s = time.perf_counter() - t1
+        eo = float(np.abs(o[b, h].double().cpu().numpy() - ro).max())
+        el = float(np.abs(lse[b, h].double().cpu().numpy() - rl).max())
+        worst_o, worst_l = max(worst_o, eo), max(worst_l, el)
+        _record(config=name, shape=list(shape), dtype="bf16" if dt == O.BF16 else "f16",
+                bh=bh, max_abs_o=eo, max_abs_lse=el, o_tol=O_TOL[dt], lse_tol=LSE_TOL,
+                oracle_o="reference sdpa_tiled AccumMode::F64 {128,128,2,col} (oracle/_ref)",
+                oracle_lse="row-blocked float64 restatement", gpu_call_s=gpu_s,
+                reference_s=ref_s)
+        assert eo <= O_TOL[dt], (name, bh, eo)
+        assert el <= LSE_TOL, (name, bh, el)
+    assert bool(torch.isfinite(o).all()) and bool(torch.isfinite(lse).all())
+    del q, k, v, o, lse
+    torch.cuda.empty_cache()
+
+
+def test_exp2_emulation_kat_against_reference_fast_expf(ta, cuda_device):
+    """ex2_poly2 (FMA-pipe exp2, row a6) against the reference's fast_expf
+    known answers (tests/golden/golden.json, generated from oracle/_ref by
+    make_golden.py): exp(x) = 2^(x log2 e).  ex2_poly2 is a degree-3
+    polynomial (max rel. error 1.0e-4 on [-0.5, 0.5] after the split), the
+    reference's fast_expf a degree-7 one (rel. error <= 1e-6,
+    test_tiled.cpp:37-49): the KAT bound is the emulation's own 1.2e-4 plus
+    fp32 rounding of x log2 e.  MUFU ex2 is checked the same way."""
+    import torch
+    from pathlib import Path
+    gold = json.loads((Path(__file__).resolve().parent / "golden" / "golden.json").read_text())
+    x = np.asarray(gold["fast_expf"]["x"], np.float32)
+    y_ref = np.asarray(gold["fast_expf"]["y"], np.float64)
+    # the softmax only exponentiates x <= 0 (scores minus the running max,
+    # bounded above by the lazy-rescale threshold 2^8): keep that domain
+    assert (x <= 0).all()
+    xd = torch.from_numpy(x * np.float32(1.4426950408889634)).cuda()
+    for mode, rel in ((0, 1.3e-4), (1, 2e-6)):
+        yd = torch.empty_like(xd)
+        stream = torch.cuda.current_stream().cuda_stream
+        rc = ta.lib().ta_debug_exp2(xd.data_ptr(), yd.data_ptr(), xd.numel(), mode, stream)
+        assert rc == 0, ta.lib().ta_last_error()
+        y = yd.double().cpu().numpy()
+        big = y_ref > 1e-30  # normal results: relative error
+        relerr = np.abs(y[big] - y_ref[big]) / y_ref[big]
+        # + the fp32 rounding of x log2 e (half an ulp of |x| log2 e, times ln 2)
+        bound = rel + np.abs(x[big]).astype(np.float64) * 1.4427 * 2.0 ** -24 * 0.6932
+        assert (relerr <= bound).all(), (mode, float((relerr - bound).max()))
+        # results the reference flushes (x < -87 -> 0) stay ~0 here too
+        assert np.abs(y[~big]).max(initial=0.0) <= 1e-30
+        _record(config="exp2_kat", mode=["ex2_poly2", "mufu_ex2"][mode],
+                n=int(x.size), max_rel=float(relerr.max()), tol=rel)
+    # exact anchor points: 2^0 = 1 and integer powers are exact on both units
+    xi = torch.tensor([0.0, -1.0, -2.0, -10.0, -126.0, 1.0, 7.0], device="cuda")
+    for mode in (0, 1):
+        yd = torch.empty_like(xi)
+        rc = ta.lib().ta_debug_exp2(xi.data_ptr(), yd.data_ptr(), xi.numel(), mode,
+                                    torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        assert yd.cpu().tolist()[:4] == [1.0, 0.5, 0.25, 2.0 ** -10]
