@@ -130,9 +130,13 @@ std::shared_ptr<const Plan> get_plan(const ta_schedule& s, int64_t d, ta_dtype d
       return it->second;
     }
   }
-  auto g = ta::fwd_geometry(1, 1, d);
+  // the schedule's t_n selects the executed K/V tile (64 keys for t_n <= 64
+  // where a 64-key kernel exists, else 128); t_m is a hint: the tcgen05 M
+  // tile is 128 rows (two per CTA at D <= 128)
+  const int bn = ta::fwd_block_n(d, s.t_n);
+  auto g = ta::fwd_geometry(1, 1, d, bn);
   auto plan = std::make_shared<const Plan>(
-      Plan{g.block_m, g.block_n, ta::fwd_ring_slots(int(d)), g.q_tiles_per_cta, g.threads});
+      Plan{g.block_m, g.block_n, ta::fwd_ring_slots(int(d), bn), g.q_tiles_per_cta, g.threads});
   c.constructions.fetch_add(1, std::memory_order_relaxed);
   std::lock_guard<std::mutex> lock(c.mu);
   auto [it, inserted] = c.plans.emplace(key, std::move(plan));
@@ -253,7 +257,7 @@ void fill_stats(ta_kernel_stats* st, const Plan& p, ta_shape sh, ta_mask_kind ma
   const int64_t bh = sh.b * sh.h;
   const int64_t q_tiles = (sh.s + p.block_m - 1) / p.block_m;
   const int64_t kv_tiles = (sh.s + p.block_n - 1) / p.block_n;
-  const auto g = ta::fwd_geometry(sh.s, bh, sh.d);
+  const auto g = ta::fwd_geometry(sh.s, bh, sh.d, p.block_n);
   uint64_t visited = 0;
   if (mask == TA_MASK_CAUSAL) {
     for (int64_t qt = 0; qt < q_tiles; ++qt) {
@@ -409,6 +413,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   }
   L.bh = bh;
   L.head_dim = ta::fwd_kernel_head_dim(sh.d);  // kernel instantiation
+  L.block_n = plan.block_n;
   L.args.head_dim = int(sh.d);         // row length of q/k/v/o in memory
   L.bf16 = bf16;
   L.stream = stream;

@@ -35,7 +35,8 @@ namespace ta {
 namespace {
 
 constexpr int kBM = 128;        // rows per Q tile (UMMA M)
-constexpr int kBN = 128;        // keys per K/V tile (UMMA N of QK^T, K of PV)
+constexpr int kBN128 = 128;     // default keys per K/V tile (UMMA N of QK^T, K of PV);
+                                // the kernels take kBN (128, or 64 for t_n <= 64 at D=128)
 constexpr int kQTiles = 2;      // max Q tiles per CTA (ping-pong)
 
 // Warp roles and register split of a CTA with kQT Q tiles (kQT = 2: the
@@ -46,9 +47,11 @@ constexpr int kQTiles = 2;      // max Q tiles per CTA (ping-pong)
 // high ids, so the single-thread roles are never starved).
 // kWide (D > 128): one Q tile, one CTA per SM (the O accumulator needs up
 // to 256 TMEM columns), no register rebalancing (255 registers per thread).
-template <int kQT, bool kWide = false>
+template <int kQT, bool kWide = false, bool kSplit = false>
 struct Roles {
-  static constexpr int kSoftmaxWarps = 4 * kQT;
+  // kSplit: two softmax warps per TMEM lane quadrant and Q tile, each owning
+  // 64 of the tile's 128 key columns
+  static constexpr int kSoftmaxWarps = 4 * kQT * (kSplit ? 2 : 1);
   static constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
   static constexpr int kMinBlocks = kQT == 1 && !kWide ? 2 : 1;
   static constexpr bool kSetMaxNReg = !kWide;
@@ -62,8 +65,9 @@ struct Roles {
   // (kQT=2: 65536/384 -> 168, 256*(208-168) == 128*(168-88); kQT=1, two
   // CTAs: 32768/256 -> 128, 128*(200-128) == 128*(128-56)).
   static constexpr int kLaunchRegs = kWide ? 248 : (65536 / (kThreads * kMinBlocks)) & ~7;
-  static constexpr int kRegsSoftmax = kWide ? 248 : kQT == 1 ? 200 : 208;
-  static constexpr int kRegsControl = kWide ? 248 : kQT == 1 ? 56 : 88;
+  // (kSplit: 640 threads -> 96; 512 * (104 - 96) <= 128 * (96 - 56))
+  static constexpr int kRegsSoftmax = kWide ? 248 : kSplit ? 104 : kQT == 1 ? 200 : 208;
+  static constexpr int kRegsControl = kWide ? 248 : kSplit ? 56 : kQT == 1 ? 56 : 88;
   static_assert(kSoftmaxWarps * 32 * (kRegsSoftmax - kLaunchRegs) <=
                     (kThreads - kSoftmaxWarps * 32) * (kLaunchRegs - kRegsControl),
                 "setmaxnreg.inc would wait forever: register pool does not balance");
@@ -77,8 +81,14 @@ struct Roles {
 #endif
 template <int D>
 constexpr int kQTilesFor = D == 64 ? TA_D64_TILES : D == 128 ? TA_D128_TILES : 1;
+// D=128 softmax split over two warps per lane quadrant and tile (TA_D128_SPLIT)
+#ifndef TA_D128_SPLIT
+#define TA_D128_SPLIT 1
+#endif
 template <int D, int kQT>
-using RolesFor = Roles<kQT, (D > 128)>;
+constexpr bool kSplitFor = TA_D128_SPLIT && D == 128 && kQT == 2;
+template <int D, int kQT>
+using RolesFor = Roles<kQT, (D > 128), kSplitFor<D, kQT>>;
 constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
@@ -90,6 +100,11 @@ constexpr float kRescaleThreshold = 8.0f;
 // pipe (same-box A/B in profiles/r01/microbench.md).
 #ifndef TA_EMU16_D128
 #define TA_EMU16_D128 0
+#endif
+// split softmax (D=128): a quarter of the exps on the FMA pipe keeps the
+// four softmax warps per SMSP below the MUFU pipe's 8 cycles per warp-exp
+#ifndef TA_EMU16_SPLIT
+#define TA_EMU16_SPLIT 4
 #endif
 #ifndef TA_EMU16_D64
 #define TA_EMU16_D64 4
@@ -107,6 +122,13 @@ constexpr int kPParts = TA_P_PARTS;
 #endif
 constexpr bool kStaleMax = TA_STALE_MAX != 0;
 constexpr float kSumGuard = 256.0f;
+// every completed mbarrier phase is waited on by some thread (the slow-path
+// barriers o_full / o_half included), so compute-sanitizer synccheck sees no
+// unobserved phase
+#ifndef TA_OBSERVE_PHASES
+#define TA_OBSERVE_PHASES 1
+#endif
+constexpr bool kObservePhases = TA_OBSERVE_PHASES != 0;
 
 #ifndef TA_SLOTS_D128
 #define TA_SLOTS_D128 4
@@ -127,18 +149,26 @@ constexpr bool kTmaStoreO = TA_TMA_STORE_O != 0;
 #define TA_D64_ROT 1
 #endif
 
-template <int D, int kQT = kQTilesFor<D>>
+template <int D, int kQT = kQTilesFor<D>, int kBN = kBN128>
 struct Cfg {
   static constexpr int kRegions = D / 64;                   // 128-B swizzle atoms along D
   static constexpr int kTileBytes = kBM * D * 2;            // one Q / K / V tile
   static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
+  static constexpr int kKVBytes = kBN * D * 2;              // one K / V tile
+  static constexpr int kKVRegionBytes = kBN * 128;          // kBN rows x 128 B
+  static_assert(kBN == 128 || (kBN == 64 && D == 128 && kQT == 2),
+                "64-key tiles: the D=128 split-softmax kernel only");
   // K/V ring depth (two CTAs per SM at kQT = 1: 16 KB Q + 4 x 16 KB ring each)
   // (D > 128: Q + 3 x 48 KB or 2 x 64 KB = 192 KB, one CTA per SM)
   static constexpr int kSlots = D > 128 ? (D == 192 ? 3 : 2)
-                                : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128)
+                                : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128 * (128 / kBN))
                                 : kQT == 1 ? TA_SLOTS_D64 : 8;
-  static constexpr int kSmemData = kQT * kTileBytes + kSlots * kTileBytes;
-  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + 1024 /*align pad*/;
+  static constexpr bool kSplit = kSplitFor<D, kQT>;
+  static constexpr int kSmemData = kQT * kTileBytes + kSlots * kKVBytes;
+  // (kSplit: + 4 KB of per-row exchange between the two warps of a row:
+  // [max | l][Q tile][lane quadrant][column half][lane] floats)
+  static constexpr int kSmemXch = kSplit ? 2 * kQT * 4 * 2 * 32 * 4 : 0;
+  static constexpr int kSmemBytes = kSmemData + 1024 /*barriers*/ + kSmemXch + 1024 /*align pad*/;
   // S/P rotation (D=64, kQT=1): TMEM units U0 = [0,64), U1 = [64,128),
   // U2 = [128,192), O at [192,256).  S(j) occupies U0U1 (j even) or U1U2 (j
   // odd) and P(j) its unit U0 (even) or U2 (odd), so S(j+1) never touches
@@ -175,13 +205,13 @@ struct Barriers {
   uint32_t tmem_base;
 };
 
-template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>>
+template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>, int kBN = kBN128>
 __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::kMinBlocks)
     sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v,
                     const __grid_constant__ CUtensorMap tmap_o, FwdArgs args) {
-  using C = Cfg<D, kQT>;
+  using C = Cfg<D, kQT, kBN>;
   using R = RolesFor<D, kQT>;
   constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
                 kWarpMma = R::kWarpMma;
@@ -189,7 +219,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
   // off the softmax of every K/V tile after the first (D=128 +2.3%, D=64
   // with the S/P rotation +4.5%, same-box A/B)
   constexpr bool kStale = kStaleMax;
-  constexpr int kEmu16 = D == 64 ? TA_EMU16_D64 : TA_EMU16_D128;
+  constexpr int kEmu16 = D == 64 ? TA_EMU16_D64 : C::kSplit ? TA_EMU16_SPLIT : TA_EMU16_D128;
   static_assert(kEmu16 % 2 == 0 && kEmu16 >= 0 && kEmu16 <= 16, "emulated pairs per 16 columns");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -218,11 +248,12 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
       : args.valid_len_dev != nullptr ? args.valid_len_dev[(args.bh_offset + bh) / args.heads]
                                       : args.valid_len[(args.bh_offset + bh) / args.heads];
   const int n_kv_seq = (kv_len + kBN - 1) / kBN;
-  const int diag0 = q0 / kBN;  // K/V tile on Q tile 0's diagonal
+  const int diag0 = q0 / kBN;  // K/V tile on Q tile 0's diagonal (kBN = 128)
   int n_kv_t[kQTiles] = {0, 0};
 #pragma unroll
-  for (int t = 0; t < kQT; ++t)
-    n_kv_t[t] = args.mask == kMaskCausal ? min(diag0 + t + 1, n_kv_seq) : n_kv_seq;
+  for (int t = 0; t < kQT; ++t)  // causal: up to the tile holding Q tile t's last row
+    n_kv_t[t] = args.mask == kMaskCausal ? min((q0 + (t + 1) * kBM - 1) / kBN + 1, n_kv_seq)
+                                         : n_kv_seq;
   const int n_kv = n_kv_t[kQT - 1];  // K/V tiles streamed (max over the Q tiles)
   long long* const trace = (kTrace && blockIdx.x == 0) ? args.trace : nullptr;
   auto rec = [&](int ev, int j) {
@@ -247,9 +278,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
     ring_tile(p, kv, j);
     const int slot = p % C::kSlots;
     const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-    mbar_arrive_expect_tx(fbar, C::kTileBytes);
+    mbar_arrive_expect_tx(fbar, C::kKVBytes);
     for (int r = 0; r < C::kRegions; ++r)
-      tma_load_3d(sring + slot * C::kTileBytes + r * C::kRegionBytes, kv == 0 ? &tmap_k : &tmap_v,
+      tma_load_3d(sring + slot * C::kKVBytes + r * C::kKVRegionBytes, kv == 0 ? &tmap_k : &tmap_v,
                   fbar, r * 64, j * kBN, bh);
   };
   // The TMA thread initialises the barriers and issues Q and the first ring
@@ -347,19 +378,20 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
       // field (addr >> 4; smem addresses < 256 KB never carry out of 14 bits)
       const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
       const uint64_t kvdesc_k = sdesc_sw128(sring, 16, 1024);
-      const uint64_t kvdesc_v = sdesc_sw128(sring, C::kRegionBytes, 1024);
+      const uint64_t kvdesc_v = sdesc_sw128(sring, C::kKVRegionBytes, 1024);
       auto issue_qk = [&](int t, int r, uint32_t scol = 0) {
         uint64_t qd = qdesc + uint64_t((t * C::kTileBytes) >> 4);
-        uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+        uint64_t kd = kvdesc_k + uint64_t((slot_of(r) * C::kKVBytes) >> 4);
         const uint32_t dS = tmem + C::kTmemS + t * kBN + scol;
 #pragma unroll
         for (int r = 0; r < C::kRegions; ++r) {  // 4 K-steps of 16 per 128-B swizzle region
-          const uint32_t off = (r * C::kRegionBytes) >> 4;
+          const uint32_t off = (r * C::kRegionBytes) >> 4;      // Q region r
+          const uint32_t koff = (r * C::kKVRegionBytes) >> 4;  // K region r
           if (D <= 128 || n_kstep >= 4 * r + 4) {
-            umma_ss_x4<2, 2>(dS, qd + off, kd + off, idesc_qk, r > 0);
+            umma_ss_x4<2, 2>(dS, qd + off, kd + koff, idesc_qk, r > 0);
           } else {  // head dim below the kernel's: skip the all-zero K-steps
             for (int ks = 0; ks < n_kstep - 4 * r; ++ks)
-              umma_ss_warp(dS, qd + off + 2 * ks, kd + off + 2 * ks, idesc_qk, (r > 0 || ks > 0));
+              umma_ss_warp(dS, qd + off + 2 * ks, kd + koff + 2 * ks, idesc_qk, (r > 0 || ks > 0));
           }
         }
         umma_commit_warp(smem_u32(&bars->s_full[t]));
@@ -368,23 +400,36 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
       // warpgroup has written that half of P (P aliases S in TMEM).
       auto issue_pv = [&](int t, int r, bool accumulate, int j) {
         const uint32_t tP = tmem + C::kTmemS + t * kBN + C::p_col(j);
-        uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kTileBytes) >> 4);
+        uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kKVBytes) >> 4);
 #pragma unroll
         for (int h = 0; h < kPParts; ++h) {
           mbar_wait_ctrl(smem_u32(&bars->p_full[C::p_bar(t, j)][h]), C::p_parity(j));
           tc_fence_after();
           if (h == kPParts - 1 && lane == 0) rec(t == 0 ? kEvMmaWaitP0 : kEvMmaWaitP1, j);
-          static_assert((kBN / 16 / kPParts) % 4 == 0, "P part = 4k K-steps of 16 keys");
+          static_assert((kBN / 16 / kPParts) % 2 == 0, "P part = 2k K-steps of 16 keys");
           constexpr int kSteps = kBN / 16 / kPParts;
+          constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
+          // P columns: 8 per K-step of 16 keys; split softmax: part h (one
+          // warp's kBN / 2 keys) over the first kBN / 4 S columns of its half
+          const uint32_t tPh = tP + (C::kSplit ? h * (kBN / 2 - kSteps * 8) : 0);
+          if constexpr (kSteps % 4 == 0) {
 #pragma unroll
-          for (int g = 0; g < kSteps / 4; ++g) {
-            const int ks0 = h * kSteps + g * 4;
-            constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
-            umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tP + ks0 * 8,
-                               vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv_n,
-                               (accumulate || ks0 > 0) ? 1u : 0u);
+            for (int g = 0; g < kSteps / 4; ++g) {
+              const int ks0 = h * kSteps + g * 4;
+              umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tPh + ks0 * 8,
+                                 vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv_n,
+                                 (accumulate || ks0 > 0) ? 1u : 0u);
+            }
+          } else {
+#pragma unroll
+            for (int g = 0; g < kSteps / 2; ++g) {
+              const int ks0 = h * kSteps + g * 2;
+              umma_ts_x2<kVStep>(tmem + C::kTmemO + t * D, tPh + ks0 * 8,
+                                 vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv_n,
+                                 (accumulate || ks0 > 0) ? 1u : 0u);
+            }
           }
-          if (kStale && h == 0) umma_commit_warp(smem_u32(&bars->o_half[t]));
+          if (kStale && h == 0 && !C::kSplit) umma_commit_warp(smem_u32(&bars->o_half[t]));
         }
         umma_commit_warp(smem_u32(&bars->o_full[t]));
         if (lane == 0) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
@@ -476,6 +521,227 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
       }
     }
   }
+  } else if constexpr (C::kSplit) {
+    // --------------------------------------------------- softmax, split rows
+    // Two warps per TMEM lane quadrant and Q tile: warp w owns tile t = w / 8,
+    // quadrant w % 4 (rows 32 (w % 4) + lane) and key columns [64 c, 64 c + 64)
+    // of each 128-key tile, c = (w / 4) % 2.  Per SMSP that is four softmax
+    // warps (both tiles, both halves): a tile's 128 exps per row are issued by
+    // two warps at once, which halves the per-warp MUFU issue chain that bounds
+    // the one-warp-per-row softmax (profiles/r02/microbench.md).  The two warps
+    // of a row share the running max: exact on the first tile (exchanged
+    // through shared memory), stale afterwards with the half-row sums voted
+    // (bar.red.or) so both halves take the slow path together.  Each keeps its
+    // own partial l; P of its 64 keys goes over its own first 32 S columns
+    // (16-bit pairs); the epilogue normalises its half of the O columns.
+    if constexpr (R::kSetMaxNReg)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R::kRegsSoftmax));
+    const int t = int(warp) / 8;
+    const int c = int(warp / 4) & 1;
+    const uint32_t wq = warp & 3;
+    const int row = int(wq * 32 + lane);
+    const uint32_t lane_off = (wq * 32u) << 16;
+    constexpr int kHalf = kBN / 2;  // key columns per warp
+    const uint32_t tS = tmem + lane_off + C::kTmemS + t * kBN + kHalf * c;  // its S columns
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D + (D / 2) * c;  // its O columns
+    const float sl2 = args.scale_log2;
+    const uint32_t sbar = smem_u32(&bars->s_full[t]);
+    const uint32_t obar = smem_u32(&bars->o_full[t]);
+    const uint32_t pbar = smem_u32(&bars->p_full[t][c]);
+    const uint32_t pair_bar = 1 + t * 4 + wq;  // named barrier of the row's two warps
+    // exchange slots [max|l][t][wq][c][lane]
+    float* xch = reinterpret_cast<float*>(smem + C::kSmemData + 1024);
+    float* xm_mine = xch + ((t * 4 + int(wq)) * 2 + c) * 32 + lane;
+    float* xm_other = xch + ((t * 4 + int(wq)) * 2 + (c ^ 1)) * 32 + lane;
+    constexpr int kXL = 2 * 4 * 2 * 32;  // offset of the l slots
+    auto pair_max = [&](float v) {
+      *xm_mine = v;
+      named_bar_sync(pair_bar, 64);
+      return fmaxf(v, *xm_other);
+    };
+    constexpr int kEmu = kEmu16;
+    float m_run = -INFINITY;  // shared by the row's two warps (scaled, log2 units)
+    float l_run = 0.f;        // this warp's partial normaliser over its columns
+    const int my_n_kv = n_kv_t[t];
+    const uint64_t sl2x2 = f2(sl2, sl2);
+
+    auto load_s = [&](float (&sv)[kHalf], int j) {
+      uint32_t sr[kHalf / 32][32];
+#pragma unroll
+      for (int h = 0; h < kHalf / 32; ++h) tmem_ld32(tS + 32 * h, sr[h]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int h = 0; h < kHalf / 32; ++h) reg_fence(sr[h]);
+#pragma unroll
+      for (int h = 0; h < kHalf / 32; ++h)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[h * 32 + i] = __uint_as_float(sr[h][i]);
+      // last admitted key of this row in the tile (ragged tail / padding /
+      // causal: key j kBN + i admitted iff <= query q0 + 128 t + row); column
+      // i here is key kHalf c + i of the tile
+      int lim = kBN - 1;
+      if (j == n_kv_seq - 1) lim = min(lim, kv_len - j * kBN - 1);
+      if (args.mask == kMaskCausal) lim = min(lim, q0 + t * kBM + row - j * kBN);
+      lim -= kHalf * c;
+      if (lim < kHalf - 1) {
+#pragma unroll
+        for (int i = 0; i < kHalf; ++i)
+          if (i > lim) sv[i] = -INFINITY;
+      }
+    };
+    // exps of the warp's 64 columns against m_use: P packed into pk, sum
+    auto exps = [&](const float (&sv)[kHalf], float m_use, uint32_t (&pk)[kHalf / 2]) {
+      const uint64_t negm2 = f2(-m_use, -m_use);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+      for (int g = 0; g < kHalf / 8; ++g) {  // groups of 8 columns
+        const int c0 = g * 8;
+        const int emu_pairs = (g & 1) ? kEmu / 4 : kEmu / 2 - kEmu / 4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t x = ffma2(f2(sv[c0 + 2 * u], sv[c0 + 2 * u + 1]), sl2x2, negm2);
+          float p0, p1;
+          if (u >= 4 - emu_pairs) {
+            ex2_poly2(x, p0, p1);
+          } else {
+            float a, b;
+            f2_split(x, a, b);
+            p0 = ex2(a);
+            p1 = ex2(b);
+          }
+          acc[u] = fadd2(acc[u], f2(p0, p1));
+          pk[g * 4 + u] = pack2<kBF16>(p0, p1);
+        }
+      }
+      float lo, hi;
+      f2_split(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), lo, hi);
+      return lo + hi;
+    };
+
+    for (int j = 0; j < my_n_kv; ++j) {
+      mbar_wait(sbar, uint32_t(j & 1));
+      tc_fence_after();
+      const bool tr = kTrace && row == TA_TRACE_ROW && c == 0;
+      if (tr) rec(kEvSm0SReady + 5 * t, j);
+      float sv[kHalf];
+      load_s(sv, j);
+      if (tr) rec(kEvSm0Loaded + 5 * t, j);
+      if (j == 0) {
+        // first tile: the exact row max over both halves (no O yet)
+        float mx4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mx4[i] = sv[i];
+#pragma unroll
+        for (int i = 4; i < kHalf; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], sv[i]);
+        const float mx = pair_max(fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
+        m_run = mx * sl2;
+        if (tr) rec(kEvSm0Max + 5 * t, j);
+      }
+      float m_use = m_run == -INFINITY ? 0.f : m_run;
+      uint32_t pk[kHalf / 2];
+      float psum = exps(sv, m_use, pk);
+      if (tr) rec(kEvSm0Exp + 5 * t, j);
+      // stale max: if some p of either half may exceed 2^8 (sum > 2^8, inf or
+      // NaN), both warps move m to the row's true max, rescale l and their O
+      // columns (after PV(j-1) has landed; PV(j) waits for this P) and redo
+      if (j > 0 && named_bar_or(pair_bar, 64, !(psum <= kSumGuard))) {
+        load_s(sv, j);  // S(j) is intact: P(j) is not written yet
+        float mx4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mx4[i] = sv[i];
+#pragma unroll
+        for (int i = 4; i < kHalf; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], sv[i]);
+        const float m_new = pair_max(fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]))) * sl2;
+        const bool need = m_new > m_run;
+        const float alpha = need ? ex2(m_run - m_new) : 1.f;
+        if (need) {
+          l_run *= alpha;
+          m_run = m_new;
+          m_use = m_run;
+        }
+        mbar_wait(obar, uint32_t((j - 1) & 1));
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < D / 2; cc += 16) {
+          uint32_t orow[16];
+          tmem_ld16(tO + cc, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+          tmem_st16(tO + cc, orow);
+        }
+        psum = exps(sv, m_use, pk);
+      }
+      l_run += psum;
+      // observe o_full's phase j-1 (PV(j-1)) before P(j) lets PV(j) complete
+      // phase j: S(j) was issued after PV(j-1), so it has completed (one
+      // test_wait).  Only the slow path needs o_full, but an unobserved phase
+      // is what compute-sanitizer synccheck reports ("missing wait").
+      if (kObservePhases && j > 0 && lane == 0) mbar_observe(obar, uint32_t((j - 1) & 1));
+#pragma unroll
+      for (int i = 0; i < kHalf / 32; ++i)
+        tmem_st16(tS + 16 * i, *reinterpret_cast<uint32_t(*)[16]>(&pk[16 * i]));
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pbar);
+      if (tr) rec(kEvSm0PArrive + 5 * t, j);
+      // warp skew of tile 0 (trace builds): W1 = the row partner (wq 0, c 1),
+      // W2 / W3 = the two warps on the MMA warp's SMSP (wq 3, c 0 / 1)
+      if (kTrace && t == 0 && lane == TA_TRACE_ROW && (wq == 0 ? c == 1 : wq == 3))
+        rec(wq == 0 ? kEvSm0ArriveW1 : kEvSm0ArriveW2 + c, j);
+    }
+
+    // ------------------------------------------------------ epilogue (split)
+    if (my_n_kv > 0) {
+      mbar_wait(obar, uint32_t((my_n_kv - 1) & 1));
+      tc_fence_after();
+    }
+    xch[kXL + ((t * 4 + int(wq)) * 2 + c) * 32 + lane] = l_run;
+    named_bar_sync(pair_bar, 64);
+    const float l_tot = l_run + xch[kXL + ((t * 4 + int(wq)) * 2 + (c ^ 1)) * 32 + lane];
+    const int grow = q0 + t * kBM + row;
+    const float inv_l = l_tot > 0.f ? 1.f / l_tot : 0.f;
+    const int dm = args.head_dim;
+    const uint32_t so = sq + t * C::kTileBytes + c * C::kRegionBytes;  // its 64 O columns
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t orow[32];
+      if (my_n_kv > 0) {
+        tmem_ld32(tO + h * 32, orow);
+        tmem_wait_ld();
+        reg_fence(orow);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) orow[i] = 0u;
+      }
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
+                                 __uint_as_float(orow[2 * i + 1]) * inv_l);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // 16-B chunk k of the row's 128-B line, XOR row % 8
+        const uint32_t k = uint32_t(h * 4 + i);
+        st_shared_v4(so + row * 128 + ((k ^ (row & 7)) << 4), packed[4 * i], packed[4 * i + 1],
+                     packed[4 * i + 2], packed[4 * i + 3]);
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(9 + t, 2 * kBM);  // the tile's eight softmax warps
+    if (row == 0 && c == 0) {
+      for (int r = 0; r < C::kRegions; ++r)
+        if (r * 64 < dm) tma_store_3d(&tmap_o, sq + t * C::kTileBytes + r * C::kRegionBytes, r * 64,
+                                      q0 + t * kBM, bh);
+      tma_store_commit();
+    }
+    if (c == 0 && args.lse != nullptr && grow < S)
+      args.lse[size_t(bh) * S + grow] =
+          l_tot > 0.f ? (m_run + __log2f(l_tot)) * kLn2 : -INFINITY;
+    if (row == 0 && c == 0) tma_store_wait_read0();
+    if (kTrace && row == 0 && c == 0) rec(kEvEpilogueDone, t);
   } else {
     // -------------------------------------------------------------- softmax
     if constexpr (R::kSetMaxNReg)
@@ -496,6 +762,14 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
     const int my_n_kv = n_kv_t[t];
     for (int j = 0; j < my_n_kv; ++j) {
       mbar_wait(sbar, uint32_t(j & 1));
+      // observe PV(j-1)'s o_full / o_half phases (synccheck "missing wait"):
+      // without the rotation S(j) follows PV(j-1) in issue order, so both are
+      // complete (never blocks); with it (S(j+1) is issued before PV(j)) this
+      // happens before P(j)'s first hand-off, below
+      if (kObservePhases && !C::kRot && j > 0 && lane == 0) {
+        mbar_observe(obar, uint32_t((j - 1) & 1));
+        if (kStale) mbar_observe(smem_u32(&bars->o_half[t]), uint32_t((j - 1) & 1));
+      }
       tc_fence_after();
       const bool tr = kTrace && row == TA_TRACE_ROW;
       if (tr) rec(kEvSm0SReady + 5 * t, j);
@@ -675,6 +949,13 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
+        if (kObservePhases && C::kRot && h == 0 && j > 0 && lane == 0) {
+          // rotation: observe PV(j-1)'s o_full / o_half phases before P(j)
+          // can let PV(j) complete the next ones (parity stays unambiguous;
+          // PV(j-1) depends only on P(j-1), already handed off)
+          mbar_observe(obar, uint32_t((j - 1) & 1));
+          if (kStale) mbar_observe(smem_u32(&bars->o_half[t]), uint32_t((j - 1) & 1));
+        }
         if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[C::p_bar(t, j)][h]));
         if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
         if (kTrace && h == kPParts - 1 && t == 0 && wq > 0 && lane == 0)
@@ -863,12 +1144,12 @@ __global__ void exp2_unit_kernel(const float* __restrict__ x, float* __restrict_
   if (i + 1 < n) y[i + 1] = p1;
 }
 
-template <int D, bool kBF16>
+template <int D, bool kBF16, int kBN = kBN128>
 cudaError_t launch_typed(const FwdLaunch& L) {
   constexpr int kQT = kQTilesFor<D>;
-  using C = Cfg<D, kQT>;
-  auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true, kQT>
-                                      : sdpa_fwd_kernel<D, kBF16, false, kQT>;
+  using C = Cfg<D, kQT, kBN>;
+  auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true, kQT, kBN>
+                                      : sdpa_fwd_kernel<D, kBF16, false, kQT, kBN>;
   static bool attr_set[64][2] = {};  // per device, per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
@@ -890,18 +1171,27 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 
 }  // namespace
 
-FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D) {
+// 64-key K/V tiles exist for the D=128 split-softmax kernel (TileSchedule
+// t_n <= 64, reference tiled.hpp:26-37); every other kernel runs 128 keys
+constexpr bool kHasBN64 = kSplitFor<128, kQTilesFor<128>>;
+
+int fwd_block_n(int64_t D, int t_n) { return kHasBN64 && D > 64 && D <= 128 && t_n <= 64 ? 64 : 128; }
+
+FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D, int block_n) {
   const int qt = D <= 64 ? kQTilesFor<64> : D <= 128 ? kQTilesFor<128> : 1;  // NOLINT
   FwdGeometry g;
   g.block_m = kBM;
-  g.block_n = kBN;
+  g.block_n = block_n;
   g.q_tiles_per_cta = qt;
-  g.threads = qt == 1 ? Roles<1>::kThreads : Roles<2>::kThreads;
+  g.threads = D <= 64    ? RolesFor<64, kQTilesFor<64>>::kThreads
+              : D <= 128 ? RolesFor<128, kQTilesFor<128>>::kThreads
+                         : RolesFor<256, 1>::kThreads;
   g.ctas = ((S + kBM * qt - 1) / (kBM * qt)) * BH;
   return g;
 }
 
-int fwd_ring_slots(int D) {
+int fwd_ring_slots(int D, int block_n) {
+  if (D > 64 && D <= 128 && block_n == 64) return Cfg<128, kQTilesFor<128>, (kHasBN64 ? 64 : 128)>::kSlots;
   return D > 192 ? Cfg<256>::kSlots : D > 128 ? Cfg<192>::kSlots
          : D > 64 ? Cfg<128>::kSlots : Cfg<64>::kSlots;
 }
@@ -909,7 +1199,13 @@ int fwd_ring_slots(int D) {
 int fwd_kernel_head_dim(int64_t D) { return D <= 64 ? 64 : D <= 128 ? 128 : D <= 192 ? 192 : 256; }
 
 cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
-  if (L.head_dim == 128) return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
+  if (L.head_dim == 128) {
+    if constexpr (kHasBN64) {
+      if (L.block_n == 64)
+        return L.bf16 ? launch_typed<128, true, 64>(L) : launch_typed<128, false, 64>(L);
+    }
+    return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
+  }
   if (L.head_dim == 64) return L.bf16 ? launch_typed<64, true>(L) : launch_typed<64, false>(L);
   if (L.head_dim == 192) return L.bf16 ? launch_typed<192, true>(L) : launch_typed<192, false>(L);
   if (L.head_dim == 256) return L.bf16 ? launch_typed<256, true>(L) : launch_typed<256, false>(L);

@@ -71,6 +71,7 @@ struct FwdLaunch {
   FwdArgs args;
   int64_t bh;
   int head_dim;  // kernel instantiation: 64, 128, 192 or 256
+  int block_n;   // keys per K/V tile: 128, or 64 (head_dim 128 only)
   bool bf16;
   void* stream;
 };
@@ -83,8 +84,10 @@ struct FwdGeometry {
   int64_t ctas;
 };
 
-FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D);
-int fwd_ring_slots(int D);
+// keys per K/V tile executed for a head dim and the schedule's t_n
+int fwd_block_n(int64_t D, int t_n);
+FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D, int block_n = 128);
+int fwd_ring_slots(int D, int block_n = 128);
 // kernel instantiation for a head dim: 64, 128, 192 or 256 (memory D <= it;
 // the TMA boxes zero-fill the extra columns)
 int fwd_kernel_head_dim(int64_t D);

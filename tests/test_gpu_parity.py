@@ -486,3 +486,56 @@ def test_tiny_and_ragged_sequences_all_kernels(ta, cuda_device, D):
             ref = torch.softmax(s, -1) @ v.float()
             assert (o.float() - ref).abs().max().item() <= TOL[O.F16], (S, causal)
             assert (lse - torch.logsumexp(s, -1)).abs().max().item() <= LSE_TOL, (S, causal)
+
+
+# ------------------------------------------- 64-key tiles (TileSchedule t_n)
+def run_gpu_sched(ta, q, k, v, dt, schedule, causal=False, valid_len=None, stats=None,
+                  scale=None):
+    import torch
+    qd, kd, vd = (torch.from_numpy(np.ascontiguousarray(x)).to(_tdt(dt)).cuda() for x in (q, k, v))
+    o, lse = ta.sdpa(qd, kd, vd, causal=causal, scale=scale, return_lse=True, stats=stats,
+                     valid_len=valid_len, schedule=schedule)
+    torch.cuda.synchronize()
+    return o.double().cpu().numpy(), lse.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("dt", [O.F16, O.BF16])
+@pytest.mark.parametrize("mask", [O.MASK_NONE, O.MASK_CAUSAL, O.MASK_PADDING])
+@pytest.mark.parametrize("S", [1, 17, 64, 65, 129, 300, 700])
+def test_block_n_64_matches_oracle(ta, cuda_device, dt, mask, S):
+    # TileSchedule t_n <= 64 (tiled.hpp:26-37) runs the 64-key D=128 kernel:
+    # stats report it, and the output matches the oracle like the 128-key one
+    B, H, D = 2, 2, 128
+    q, k, v = O.make_input((B, H, S, D), dt, 7000 + S + 10 * mask)
+    vl = [S, max(0, S // 2 - 3)] if mask == O.MASK_PADDING else None
+    st = ta.KernelStats()
+    o, lse = run_gpu_sched(ta, q, k, v, dt, ta.TileSchedule(64, 64, 2), causal=mask == O.MASK_CAUSAL,
+                           valid_len=vl, stats=st)
+    assert st.block_n == 64 and st.block_m == 128
+    r = oracle_ref(q, k, v, mask_kind=mask, valid_len=vl)
+    assert np.abs(o - r["o"]).max() <= TOL[dt], (S, mask)
+    _check_lse(lse, r["lse"])
+
+
+def test_block_n_64_lazy_rescale_and_wide_spread(ta, cuda_device):
+    # scale 1 at D=128: the stale-max slow path (pair vote) on 64-key tiles
+    q, k, v = O.make_input((1, 2, 1024, 128), O.F16, 23)
+    o, lse = run_gpu_sched(ta, q, k, v, O.F16, ta.TileSchedule(32, 32, 1), scale=1.0)
+    r = oracle_ref(q, k, v, scale=1.0)
+    assert np.abs(o - r["o"]).max() <= TOL[O.F16]
+    assert np.abs(lse - r["lse"]).max() <= 4e-3
+
+
+@pytest.mark.parametrize("t_n,want", [(16, 64), (32, 64), (64, 64), (128, 128), (256, 128)])
+def test_schedule_selects_executed_block_n(ta, cuda_device, t_n, want):
+    q, k, v = O.make_input((1, 1, 300, 96), O.BF16, 3)
+    st = ta.KernelStats()
+    o, _ = run_gpu_sched(ta, q, k, v, O.BF16, ta.TileSchedule(64, t_n, 2), stats=st)
+    assert st.block_n == want
+    assert st.kv_tiles_visited == math.ceil(300 / 128) * math.ceil(300 / want)
+    r = oracle_ref(q, k, v)
+    assert np.abs(o - r["o"]).max() <= TOL[O.BF16]
+    # other head dims run 128-key tiles whatever the schedule says
+    q, k, v = O.make_input((1, 1, 300, 64), O.BF16, 3)
+    run_gpu_sched(ta, q, k, v, O.BF16, ta.TileSchedule(64, t_n, 2), stats=st)
+    assert st.block_n == 128
