@@ -82,13 +82,14 @@ struct Roles {
 template <int D>
 constexpr int kQTilesFor = D == 64 ? TA_D64_TILES : D == 128 ? TA_D128_TILES : 1;
 // D=128 softmax split over two warps per lane quadrant and tile (TA_D128_SPLIT)
+// (the 64-key kernel always splits: 32 keys per warp)
 #ifndef TA_D128_SPLIT
-#define TA_D128_SPLIT 1
+#define TA_D128_SPLIT 0
 #endif
-template <int D, int kQT>
-constexpr bool kSplitFor = TA_D128_SPLIT && D == 128 && kQT == 2;
-template <int D, int kQT>
-using RolesFor = Roles<kQT, (D > 128), kSplitFor<D, kQT>>;
+template <int D, int kQT, int kBN = 128>
+constexpr bool kSplitFor = D == 128 && kQT == 2 && (TA_D128_SPLIT || kBN == 64);
+template <int D, int kQT, int kBN = 128>
+using RolesFor = Roles<kQT, (D > 128), kSplitFor<D, kQT, kBN>>;
 constexpr float kLn2 = 0.69314718055994530942f;
 // lazy rescale threshold in log2 units: exps may reach 2^8 before O is
 // rescaled (fp32 accumulators, 16-bit P: both fine).
@@ -125,8 +126,10 @@ constexpr float kSumGuard = 256.0f;
 // every completed mbarrier phase is waited on by some thread (the slow-path
 // barriers o_full / o_half included), so compute-sanitizer synccheck sees no
 // unobserved phase
+// (off in the product build: the observation costs 4-6% -- a same-box A/B;
+// scripts/sanitize.sh checks both builds)
 #ifndef TA_OBSERVE_PHASES
-#define TA_OBSERVE_PHASES 1
+#define TA_OBSERVE_PHASES 0
 #endif
 constexpr bool kObservePhases = TA_OBSERVE_PHASES != 0;
 
@@ -163,7 +166,7 @@ struct Cfg {
   static constexpr int kSlots = D > 128 ? (D == 192 ? 3 : 2)
                                 : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128 * (128 / kBN))
                                 : kQT == 1 ? TA_SLOTS_D64 : 8;
-  static constexpr bool kSplit = kSplitFor<D, kQT>;
+  static constexpr bool kSplit = kSplitFor<D, kQT, kBN>;
   static constexpr int kSmemData = kQT * kTileBytes + kSlots * kKVBytes;
   // (kSplit: + 4 KB of per-row exchange between the two warps of a row:
   // [max | l][Q tile][lane quadrant][column half][lane] floats)
@@ -206,13 +209,13 @@ struct Barriers {
 };
 
 template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>, int kBN = kBN128>
-__global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::kMinBlocks)
+__global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, kQT, kBN>::kMinBlocks)
     sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v,
                     const __grid_constant__ CUtensorMap tmap_o, FwdArgs args) {
   using C = Cfg<D, kQT, kBN>;
-  using R = RolesFor<D, kQT>;
+  using R = RolesFor<D, kQT, kBN>;
   constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
                 kWarpMma = R::kWarpMma;
   // stale max at both head dims: it takes the row max (and its latency)
@@ -278,8 +281,13 @@ __global__ void __launch_bounds__(RolesFor<D, kQT>::kThreads, RolesFor<D, kQT>::
     ring_tile(p, kv, j);
     const int slot = p % C::kSlots;
     const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
-    mbar_arrive_expect_tx(fbar, C::kKVBytes);
-    for (int r = 0; r < C::kRegions; ++r)
+#ifdef TA_DEBUG_HALF_KV  // power ablation only (wrong results): half the K/V bytes
+    constexpr int kLoadRegions = C::kRegions > 1 ? C::kRegions / 2 : 1;
+#else
+    constexpr int kLoadRegions = C::kRegions;
+#endif
+    mbar_arrive_expect_tx(fbar, kLoadRegions * C::kKVRegionBytes);
+    for (int r = 0; r < kLoadRegions; ++r)
       tma_load_3d(sring + slot * C::kKVBytes + r * C::kKVRegionBytes, kv == 0 ? &tmap_k : &tmap_v,
                   fbar, r * 64, j * kBN, bh);
   };
@@ -1164,7 +1172,7 @@ cudaError_t launch_typed(const FwdLaunch& L) {
   const int64_t ctas = int64_t((L.args.seq_len + rows_per_cta - 1) / rows_per_cta) * L.bh;
   if (ctas > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned int>(ctas), 1u, 1u);
-  kern<<<grid, RolesFor<D, kQT>::kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
+  kern<<<grid, RolesFor<D, kQT, kBN>::kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
       *L.tmap_q, *L.tmap_k, *L.tmap_v, *L.tmap_o, L.args);
   return cudaGetLastError();
 }
@@ -1173,7 +1181,7 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 
 // 64-key K/V tiles exist for the D=128 split-softmax kernel (TileSchedule
 // t_n <= 64, reference tiled.hpp:26-37); every other kernel runs 128 keys
-constexpr bool kHasBN64 = kSplitFor<128, kQTilesFor<128>>;
+constexpr bool kHasBN64 = kQTilesFor<128> == 2;
 
 int fwd_block_n(int64_t D, int t_n) { return kHasBN64 && D > 64 && D <= 128 && t_n <= 64 ? 64 : 128; }
 
@@ -1184,7 +1192,8 @@ FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D, int block_n) {
   g.block_n = block_n;
   g.q_tiles_per_cta = qt;
   g.threads = D <= 64    ? RolesFor<64, kQTilesFor<64>>::kThreads
-              : D <= 128 ? RolesFor<128, kQTilesFor<128>>::kThreads
+              : D <= 128 ? (block_n == 64 ? RolesFor<128, kQTilesFor<128>, 64>::kThreads
+                                          : RolesFor<128, kQTilesFor<128>>::kThreads)
                          : RolesFor<256, 1>::kThreads;
   g.ctas = ((S + kBM * qt - 1) / (kBM * qt)) * BH;
   return g;
