@@ -87,7 +87,7 @@ constexpr int kQTilesFor = D == 64 ? TA_D64_TILES : D == 128 ? TA_D128_TILES : 1
 #define TA_D128_SPLIT 0
 #endif
 template <int D, int kQT, int kBN = 128>
-constexpr bool kSplitFor = D == 128 && kQT == 2 && (TA_D128_SPLIT || kBN == 64);
+constexpr bool kSplitFor = (D == 128 || D == 64) && kQT == 2 && (TA_D128_SPLIT || kBN == 64);
 template <int D, int kQT, int kBN = 128>
 using RolesFor = Roles<kQT, (D > 128), kSplitFor<D, kQT, kBN>>;
 constexpr float kLn2 = 0.69314718055994530942f;
@@ -713,9 +713,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
     const int grow = q0 + t * kBM + row;
     const float inv_l = l_tot > 0.f ? 1.f / l_tot : 0.f;
     const int dm = args.head_dim;
-    const uint32_t so = sq + t * C::kTileBytes + c * C::kRegionBytes;  // its 64 O columns
+    const uint32_t so = sq + t * C::kTileBytes;  // the tile's (dead) Q buffer
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < D / 64; ++h) {  // its D / 2 O columns, 32 at a time
       uint32_t orow[32];
       if (my_n_kv > 0) {
         tmem_ld32(tO + h * 32, orow);
@@ -732,9 +732,10 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
                                  __uint_as_float(orow[2 * i + 1]) * inv_l);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {  // 16-B chunk k of the row's 128-B line, XOR row % 8
-        const uint32_t k = uint32_t(h * 4 + i);
-        st_shared_v4(so + row * 128 + ((k ^ (row & 7)) << 4), packed[4 * i], packed[4 * i + 1],
-                     packed[4 * i + 2], packed[4 * i + 3]);
+        const int gcol = c * (D / 2) + h * 32 + i * 8;
+        const uint32_t k = uint32_t((gcol & 63) >> 3);
+        st_shared_v4(so + (gcol >> 6) * C::kRegionBytes + row * 128 + ((k ^ (row & 7)) << 4),
+                     packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
       }
     }
     fence_proxy_async_smem();
