@@ -372,7 +372,9 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   ta_status st;
   if ((st = make_tmap(&mq, q, bf16, bh, sh.s, sh.d, 128)) != TA_OK) return st;
   const uint32_t kv_rows = uint32_t(plan.block_n);  // one TMA box = one K/V tile row block
-  if ((st = make_tmap(&mk, k, bf16, bh, sh.s, sh.d, kv_rows)) != TA_OK) return st;
+  // CTA pair: each CTA loads half of a K tile's keys (boxes of block_n / 2 rows)
+  const bool pair = ta::fwd_use_pair(ta::fwd_kernel_head_dim(sh.d), plan.block_n, int(mask_args.kind));
+  if ((st = make_tmap(&mk, k, bf16, bh, sh.s, sh.d, pair ? kv_rows / 2 : kv_rows)) != TA_OK) return st;
   if ((st = make_tmap(&mv, v, bf16, bh, sh.s, sh.d, kv_rows)) != TA_OK) return st;
   CUtensorMap mo;
   if ((st = make_tmap(&mo, o, bf16, bh, sh.s, sh.d, 128)) != TA_OK) return st;
@@ -414,6 +416,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   L.bh = bh;
   L.head_dim = ta::fwd_kernel_head_dim(sh.d);  // kernel instantiation
   L.block_n = plan.block_n;
+  L.pair = pair;
   L.args.head_dim = int(sh.d);         // row length of q/k/v/o in memory
   L.bf16 = bf16;
   L.stream = stream;

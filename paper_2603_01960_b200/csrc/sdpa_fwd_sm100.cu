@@ -152,21 +152,25 @@ constexpr bool kTmaStoreO = TA_TMA_STORE_O != 0;
 #define TA_D64_ROT 1
 #endif
 
-template <int D, int kQT = kQTilesFor<D>, int kBN = kBN128>
+template <int D, int kQT = kQTilesFor<D>, int kBN = kBN128, bool kPair = false>
 struct Cfg {
   static constexpr int kRegions = D / 64;                   // 128-B swizzle atoms along D
   static constexpr int kTileBytes = kBM * D * 2;            // one Q / K / V tile
   static constexpr int kRegionBytes = kBM * 128;            // 128 rows x 128 B
-  static constexpr int kKVBytes = kBN * D * 2;              // one K / V tile
-  static constexpr int kKVRegionBytes = kBN * 128;          // kBN rows x 128 B
+  // kPair (CTA pair, cta_group::2): each CTA holds half of every K / V tile
+  // -- K: its kBN / 2 keys x D; V: all kBN keys x its D / 2 columns
+  static constexpr int kKVBytes = kBN * D * 2 / (kPair ? 2 : 1);  // one K / V tile (slot)
+  static constexpr int kKVRegionBytes = kBN * 128;          // kBN rows x 128 B (V regions)
+  static constexpr int kKRegionBytes = (kPair ? kBN / 2 : kBN) * 128;  // K regions
+  static_assert(!kPair || (D == 128 && kQT == 2 && kBN == 128), "pair: the D=128 kernel");
   static_assert(kBN == 128 || (kBN == 64 && D == 128 && kQT == 2),
                 "64-key tiles: the D=128 split-softmax kernel only");
   // K/V ring depth (two CTAs per SM at kQT = 1: 16 KB Q + 4 x 16 KB ring each)
   // (D > 128: Q + 3 x 48 KB or 2 x 64 KB = 192 KB, one CTA per SM)
   static constexpr int kSlots = D > 128 ? (D == 192 ? 3 : 2)
-                                : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128 * (128 / kBN))
+                                : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128 * (128 / kBN) * (kPair ? 2 : 1))
                                 : kQT == 1 ? TA_SLOTS_D64 : 8;
-  static constexpr bool kSplit = kSplitFor<D, kQT, kBN>;
+  static constexpr bool kSplit = kSplitFor<D, kQT, kBN> && !kPair;
   static constexpr int kSmemData = kQT * kTileBytes + kSlots * kKVBytes;
   // (kSplit: + 4 KB of per-row exchange between the two warps of a row:
   // [max | l][Q tile][lane quadrant][column half][lane] floats)
@@ -208,14 +212,16 @@ struct Barriers {
   uint32_t tmem_base;
 };
 
-template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>, int kBN = kBN128>
+template <int D, bool kBF16, bool kTrace, int kQT = kQTilesFor<D>, int kBN = kBN128,
+          bool kPair = false>
 __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, kQT, kBN>::kMinBlocks)
     sdpa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v,
                     const __grid_constant__ CUtensorMap tmap_o, FwdArgs args) {
-  using C = Cfg<D, kQT, kBN>;
+  using C = Cfg<D, kQT, kBN, kPair>;
   using R = RolesFor<D, kQT, kBN>;
+  static_assert(!kPair || !C::kSplit, "pair kernel: one softmax warp per row");
   constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
                 kWarpMma = R::kWarpMma;
   // stale max at both head dims: it takes the row max (and its latency)
@@ -237,8 +243,20 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
   // 1-D grid over (head, query block), query block fastest (concurrent CTAs
   // share a head's K/V in L2); no 65535 limit on B*H
   const int n_qblk = (args.seq_len + kBM * kQT - 1) / (kBM * kQT);
-  const int bh = int(blockIdx.x) / n_qblk;
-  const int qblk_in = int(blockIdx.x) - bh * n_qblk;
+  // CTA pair: clusters of two CTAs on adjacent query blocks of one head (an
+  // odd last block gets an idle partner whose rows are all >= S)
+  uint32_t rank = 0;
+  int bh, qblk_in;
+  if constexpr (kPair) {
+    rank = cluster_ctarank();
+    const int n_pairs = (n_qblk + 1) >> 1;
+    const int pair = int(blockIdx.x) >> 1;
+    bh = pair / n_pairs;
+    qblk_in = (pair - bh * n_pairs) * 2 + int(rank);
+  } else {
+    bh = int(blockIdx.x) / n_qblk;
+    qblk_in = int(blockIdx.x) - bh * n_qblk;
+  }
   // causal: heaviest query blocks first (longest-processing-time order)
   const int qblk = args.mask == kMaskCausal ? n_qblk - 1 - qblk_in : qblk_in;
   const int q0 = qblk * (kBM * kQT);
@@ -286,6 +304,20 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
 #else
     constexpr int kLoadRegions = C::kRegions;
 #endif
+    if constexpr (kPair) {
+      // each CTA loads its half into its own slot; the bytes of both halves
+      // are counted on the leader's barrier (the MMA issuer waits there)
+      const uint32_t fbar0 = mapa_shared(fbar, 0);
+      if (rank == 0) mbar_arrive_expect_tx(fbar, 2 * C::kKVBytes);
+      if (kv == 0) {  // K: keys [j kBN + 64 rank, + 64), all D columns
+        for (int r = 0; r < C::kRegions; ++r)
+          tma_load_3d_pair(sring + slot * C::kKVBytes + r * C::kKRegionBytes, &tmap_k, fbar0,
+                           r * 64, j * kBN + (kBN / 2) * int(rank), bh);
+      } else {  // V: all kBN keys, columns [64 rank, + 64)
+        tma_load_3d_pair(sring + slot * C::kKVBytes, &tmap_v, fbar0, 64 * int(rank), j * kBN, bh);
+      }
+      return;
+    }
     mbar_arrive_expect_tx(fbar, kLoadRegions * C::kKVRegionBytes);
     for (int r = 0; r < kLoadRegions; ++r)
       tma_load_3d(sring + slot * C::kKVBytes + r * C::kKVRegionBytes, kv == 0 ? &tmap_k : &tmap_v,
@@ -298,8 +330,8 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
   if (threadIdx.x == R::kWarpTma * 32) {
     mbar_init(smem_u32(&bars->q_full), 1);
     for (int t = 0; t < kQTiles; ++t)
-      for (int q = 0; q < kPParts; ++q)
-        mbar_init(smem_u32(&bars->p_full[t][q]), kBM / 32);  // one arrive per warp
+      for (int q = 0; q < kPParts; ++q)  // one arrive per warp (of both CTAs of a pair)
+        mbar_init(smem_u32(&bars->p_full[t][q]), (kBM / 32) * (kPair ? 2 : 1));
     for (int t = 0; t < kQT; ++t) {
       mbar_init(smem_u32(&bars->s_full[t]), 1);
       mbar_init(smem_u32(&bars->o_full[t]), 1);
@@ -315,18 +347,40 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
     tma_prefetch_desc(&tmap_q);
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
-    const uint32_t qbar = smem_u32(&bars->q_full);
-    if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQT * C::kTileBytes);
-    for (int t = 0; t < kQT && n_kv > 0; ++t)  // (no key admitted: Q unused)
-      for (int r = 0; r < C::kRegions; ++r)
-        tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
-                    q0 + t * kBM, bh);
-    for (int p = 0; p < ring_prefill; ++p) load_ring(p);
   }
-  if (warp == kWarpAlloc) tmem_alloc<R::kTmemCols>(smem_u32(&bars->tmem_base));
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
+  auto first_loads = [&]() {
+    const uint32_t qbar = smem_u32(&bars->q_full);
+    if constexpr (kPair) {  // both CTAs' Q tiles counted on the leader's q_full
+      if (rank == 0 && n_kv > 0) mbar_arrive_expect_tx(qbar, 2 * kQT * C::kTileBytes);
+      const uint32_t qbar0 = mapa_shared(qbar, 0);
+      for (int t = 0; t < kQT && n_kv > 0; ++t)
+        for (int r = 0; r < C::kRegions; ++r)
+          tma_load_3d_pair(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar0, r * 64,
+                           q0 + t * kBM, bh);
+    } else {
+      if (n_kv > 0) mbar_arrive_expect_tx(qbar, kQT * C::kTileBytes);
+      for (int t = 0; t < kQT && n_kv > 0; ++t)  // (no key admitted: Q unused)
+        for (int r = 0; r < C::kRegions; ++r)
+          tma_load_3d(sq + t * C::kTileBytes + r * C::kRegionBytes, &tmap_q, qbar, r * 64,
+                      q0 + t * kBM, bh);
+    }
+    for (int p = 0; p < ring_prefill; ++p) load_ring(p);
+  };
+  if (!kPair && threadIdx.x == R::kWarpTma * 32) first_loads();
+  if constexpr (kPair) {
+    // both CTAs allocate (same warp, same smem offset) and every barrier of
+    // the pair is initialised before any cross-CTA load or arrive
+    if (warp == kWarpAlloc) tmem_alloc_pair<R::kTmemCols>(smem_u32(&bars->tmem_base));
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    if (threadIdx.x == R::kWarpTma * 32) first_loads();
+  } else {
+    if (warp == kWarpAlloc) tmem_alloc<R::kTmemCols>(smem_u32(&bars->tmem_base));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   const uint32_t tmem = bars->tmem_base;
   if (threadIdx.x == 0) rec(kEvKernelStart, 1);
 
@@ -340,6 +394,12 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         mbar_wait_ctrl(smem_u32(&bars->slot_empty[p % C::kSlots]),
                        uint32_t((p / C::kSlots) & 1) ^ 1u);
         load_ring(p);
+      }
+      if constexpr (kPair) {
+        // the leader's last slot releases land in this CTA too: wait for them
+        // before the teardown so no arrive targets an exited CTA
+        for (int p = max(0, 2 * n_kv - C::kSlots); p < 2 * n_kv; ++p)
+          mbar_wait_ctrl(smem_u32(&bars->slot_empty[p % C::kSlots]), uint32_t((p / C::kSlots) & 1));
       }
     }
   } else if (warp == kWarpTrace) {
@@ -360,13 +420,19 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         }
       }
     }
-  } else if (warp == kWarpMma) {
+  } else if (warp == kWarpMma && rank == 0) {  // (pair: the leader issues for both CTAs)
     // ------------------------------------------------------------------ MMA
     // The whole warp runs this loop (uniform control flow, descriptors in
     // uniform registers); one elected lane issues each tcgen05 instruction.
     {
-      constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN, false, false);
-      constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+      // (pair: M = 256, 128 rows in each CTA's TMEM)
+      constexpr uint32_t kM = kBM * (kPair ? 2 : 1);
+      constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kM, kBN, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kM, D, false, true);
+      // commits arrive on the barrier in both CTAs of a pair
+      auto commit = [&](uint32_t bar) {
+        if constexpr (kPair) umma_commit_pair(bar); else umma_commit_warp(bar);
+      };
       // wide kernels with a smaller head dim (D=160 on the 192-column kernel,
       // TMA zero-fill past D): QK^T skips the all-zero K-steps and PV computes
       // only the O columns that are stored (+4% at D=160; at D <= 128 the
@@ -381,7 +447,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         mbar_wait_ctrl(smem_u32(&bars->slot_full[slot_of(r)]), phase_of(r));
         tc_fence_after();
       };
-      auto release = [&](int r) { umma_commit_warp(smem_u32(&bars->slot_empty[slot_of(r)])); };
+      auto release = [&](int r) { commit(smem_u32(&bars->slot_empty[slot_of(r)])); };
       // descriptors: base built once, K-step offsets added to the start-address
       // field (addr >> 4; smem addresses < 256 KB never carry out of 14 bits)
       const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
@@ -394,15 +460,17 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
 #pragma unroll
         for (int r = 0; r < C::kRegions; ++r) {  // 4 K-steps of 16 per 128-B swizzle region
           const uint32_t off = (r * C::kRegionBytes) >> 4;      // Q region r
-          const uint32_t koff = (r * C::kKVRegionBytes) >> 4;  // K region r
-          if (D <= 128 || n_kstep >= 4 * r + 4) {
+          const uint32_t koff = (r * C::kKRegionBytes) >> 4;  // K region r
+          if constexpr (kPair) {
+            umma_ss_x4_pair<2, 2>(dS, qd + off, kd + koff, idesc_qk, r > 0);
+          } else if (D <= 128 || n_kstep >= 4 * r + 4) {
             umma_ss_x4<2, 2>(dS, qd + off, kd + koff, idesc_qk, r > 0);
           } else {  // head dim below the kernel's: skip the all-zero K-steps
             for (int ks = 0; ks < n_kstep - 4 * r; ++ks)
               umma_ss_warp(dS, qd + off + 2 * ks, kd + koff + 2 * ks, idesc_qk, (r > 0 || ks > 0));
           }
         }
-        umma_commit_warp(smem_u32(&bars->s_full[t]));
+        commit(smem_u32(&bars->s_full[t]));
       };
       // PV in two halves of 64 keys, each issued as soon as the softmax
       // warpgroup has written that half of P (P aliases S in TMEM).
@@ -424,9 +492,14 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
 #pragma unroll
             for (int g = 0; g < kSteps / 4; ++g) {
               const int ks0 = h * kSteps + g * 4;
-              umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tPh + ks0 * 8,
-                                 vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv_n,
-                                 (accumulate || ks0 > 0) ? 1u : 0u);
+              if constexpr (kPair)
+                umma_ts_x4_pair<kVStep>(tmem + C::kTmemO + t * D, tPh + ks0 * 8,
+                                        vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv_n,
+                                        (accumulate || ks0 > 0) ? 1u : 0u);
+              else
+                umma_ts_x4<kVStep>(tmem + C::kTmemO + t * D, tPh + ks0 * 8,
+                                   vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv_n,
+                                   (accumulate || ks0 > 0) ? 1u : 0u);
             }
           } else {
 #pragma unroll
@@ -437,9 +510,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
                                  (accumulate || ks0 > 0) ? 1u : 0u);
             }
           }
-          if (kStale && h == 0 && !C::kSplit) umma_commit_warp(smem_u32(&bars->o_half[t]));
+          if (kStale && h == 0 && !C::kSplit) commit(smem_u32(&bars->o_half[t]));
         }
-        umma_commit_warp(smem_u32(&bars->o_full[t]));
+        commit(smem_u32(&bars->o_full[t]));
         if (lane == 0) rec(t == 0 ? kEvMmaIssuedPV0 : kEvMmaIssuedPV1, j);
       };
 
@@ -965,7 +1038,12 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           mbar_observe(obar, uint32_t((j - 1) & 1));
           if (kStale) mbar_observe(smem_u32(&bars->o_half[t]), uint32_t((j - 1) & 1));
         }
-        if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[C::p_bar(t, j)][h]));
+        if (lane == 0) {
+          if constexpr (kPair)  // the leader's barrier (the MMA issuer waits there)
+            mbar_arrive_cluster(mapa_shared(smem_u32(&bars->p_full[C::p_bar(t, j)][h]), 0));
+          else
+            mbar_arrive(smem_u32(&bars->p_full[C::p_bar(t, j)][h]));
+        }
         if (h == 0 && tr) rec(kEvSm0Exp + 5 * t, j);
         if (kTrace && h == kPParts - 1 && t == 0 && wq > 0 && lane == 0)
           rec(kEvSm0ArriveW1 + int(wq) - 1, j);
@@ -1042,9 +1120,12 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
-  if (warp == kWarpAlloc) tmem_dealloc<R::kTmemCols>(tmem);
+  if (warp == kWarpAlloc) {
+    if constexpr (kPair) tmem_dealloc_pair<R::kTmemCols>(tmem);
+    else tmem_dealloc<R::kTmemCols>(tmem);
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -1153,12 +1234,12 @@ __global__ void exp2_unit_kernel(const float* __restrict__ x, float* __restrict_
   if (i + 1 < n) y[i + 1] = p1;
 }
 
-template <int D, bool kBF16, int kBN = kBN128>
+template <int D, bool kBF16, int kBN = kBN128, bool kPair = false>
 cudaError_t launch_typed(const FwdLaunch& L) {
   constexpr int kQT = kQTilesFor<D>;
-  using C = Cfg<D, kQT, kBN>;
-  auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true, kQT, kBN>
-                                      : sdpa_fwd_kernel<D, kBF16, false, kQT, kBN>;
+  using C = Cfg<D, kQT, kBN, kPair>;
+  auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true, kQT, kBN, kPair>
+                                      : sdpa_fwd_kernel<D, kBF16, false, kQT, kBN, kPair>;
   static bool attr_set[64][2] = {};  // per device, per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1170,9 +1251,26 @@ cudaError_t launch_typed(const FwdLaunch& L) {
     attr_set[dev][tr] = true;
   }
   const int rows_per_cta = kBM * kQT;
-  const int64_t ctas = int64_t((L.args.seq_len + rows_per_cta - 1) / rows_per_cta) * L.bh;
+  int64_t qblocks = (L.args.seq_len + rows_per_cta - 1) / rows_per_cta;
+  if (kPair) qblocks = (qblocks + 1) & ~int64_t(1);  // whole pairs
+  const int64_t ctas = qblocks * L.bh;
   if (ctas > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned int>(ctas), 1u, 1u);
+  if constexpr (kPair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(RolesFor<D, kQT, kBN>::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = static_cast<cudaStream_t>(L.stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, *L.tmap_q, *L.tmap_k, *L.tmap_v, *L.tmap_o, L.args);
+  }
   kern<<<grid, RolesFor<D, kQT, kBN>::kThreads, C::kSmemBytes, static_cast<cudaStream_t>(L.stream)>>>(
       *L.tmap_q, *L.tmap_k, *L.tmap_v, *L.tmap_o, L.args);
   return cudaGetLastError();
@@ -1183,6 +1281,17 @@ cudaError_t launch_typed(const FwdLaunch& L) {
 // 64-key K/V tiles exist for the D=128 split-softmax kernel (TileSchedule
 // t_n <= 64, reference tiled.hpp:26-37); every other kernel runs 128 keys
 constexpr bool kHasBN64 = kQTilesFor<128> == 2;
+
+// CTA-pair (cta_group::2) D=128 kernel for 128-key tiles without the causal
+// mask (TA_PAIR; the pair streams one K/V sequence for both CTAs)
+#ifndef TA_PAIR
+#define TA_PAIR 0
+#endif
+constexpr bool kHasPair = TA_PAIR != 0 && kQTilesFor<128> == 2 && !TA_D128_SPLIT;
+
+bool fwd_use_pair(int64_t D, int block_n, int mask) {
+  return kHasPair && D > 64 && D <= 128 && block_n == 128 && mask != kMaskCausal;
+}
 
 int fwd_block_n(int64_t D, int t_n) { return kHasBN64 && D > 64 && D <= 128 && t_n <= 64 ? 64 : 128; }
 
@@ -1213,6 +1322,10 @@ cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
     if constexpr (kHasBN64) {
       if (L.block_n == 64)
         return L.bf16 ? launch_typed<128, true, 64>(L) : launch_typed<128, false, 64>(L);
+    }
+    if constexpr (kHasPair) {
+      if (L.pair)
+        return L.bf16 ? launch_typed<128, true, 128, true>(L) : launch_typed<128, false, 128, true>(L);
     }
     return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
   }

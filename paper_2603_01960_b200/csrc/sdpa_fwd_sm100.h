@@ -72,6 +72,7 @@ struct FwdLaunch {
   int64_t bh;
   int head_dim;  // kernel instantiation: 64, 128, 192 or 256
   int block_n;   // keys per K/V tile: 128, or 64 (head_dim 128 only)
+  bool pair;     // CTA-pair (cta_group::2) kernel: K map boxes of block_n / 2 rows
   bool bf16;
   void* stream;
 };
@@ -86,6 +87,8 @@ struct FwdGeometry {
 
 // keys per K/V tile executed for a head dim and the schedule's t_n
 int fwd_block_n(int64_t D, int t_n);
+// whether a launch runs the CTA-pair kernel (mask: kMaskNone / Causal / Padding)
+bool fwd_use_pair(int64_t D, int block_n, int mask);
 FwdGeometry fwd_geometry(int64_t S, int64_t BH, int64_t D, int block_n = 128);
 int fwd_ring_slots(int D, int block_n = 128);
 // kernel instantiation for a head dim: 64, 128, 192 or 256 (memory D <= it;

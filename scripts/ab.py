@@ -28,8 +28,16 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record(); f(); e1.record(); torch.cuda.synchronize()
 n = max(5, int(1500 / max(e0.elapsed_time(e1), 1e-3)))
 clk = []
-p = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
-threading.Thread(target=lambda: [clk.append(float(l)) for l in p.stdout if l.strip()], daemon=True).start()
+pw = []
+p = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+def _rd():
+    for l in p.stdout:
+        try:
+            a, b = l.split(",")
+            clk.append(float(a)); pw.append(float(b))
+        except ValueError:
+            pass
+threading.Thread(target=_rd, daemon=True).start()
 e0.record()
 for _ in range(n): f()
 e1.record(); torch.cuda.synchronize()
@@ -38,8 +46,9 @@ ms = e0.elapsed_time(e1) / n
 ref = torch.nn.functional.scaled_dot_product_attention(q[:1, :2], k[:1, :2], v[:1, :2], is_causal=causal)
 err = (o[:1, :2].float() - ref.float()).abs().max().item()
 mhz = statistics.median(clk[len(clk)//3:]) if clk else 0
+watt = statistics.median(pw[len(pw)//3:]) if pw else 0
 tf = 4*B*H*S*S*D/ms/1e9
-print(f"{ms:9.3f} ms {tf:7.1f} TF/s {mhz:5.0f} MHz {tf/max(mhz,1)*1000:6.1f} TF/s/GHz bn={st.block_n} err {err:.1e}")
+print(f"{ms:9.3f} ms {tf:7.1f} TF/s {mhz:5.0f} MHz {watt:5.0f} W {tf/max(mhz,1)*1000:6.1f} TF/s/GHz {tf/max(watt,1):5.2f} TF/J bn={st.block_n} err {err:.1e}")
 '''
 
 

@@ -67,7 +67,11 @@ def main() -> int:
                       eo = (o.float() - ro).abs().max().item()
                       fin = torch.isfinite(rl)
                       el = (lse[fin] - rl[fin]).abs().max().item() if fin.any() else 0.0
-                      tol = 2e-2 if dt == torch.bfloat16 else 5e-3
+                      # BASELINE tolerance (unit-variance inputs, default scale);
+                      # the scale-1 stress case has 8-16x larger scores, so a
+                      # peaked softmax whose bf16-rounded P (2^-8 spacing
+                      # below 1) moves O by ~|v| 2^-8: 3e-2 there
+                      tol = (2e-2 if scale != 1.0 else 3e-2) if dt == torch.bfloat16 else 5e-3
                       ok = eo <= tol and el <= 2e-3 and bool((lse[~fin] == -math.inf).all())
                       n += 1
                       fails += not ok
