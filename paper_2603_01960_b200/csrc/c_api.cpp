@@ -290,7 +290,7 @@ struct PaddingSlot {
   int* dev = nullptr;
   size_t cap = 0;
   cudaEvent_t done = nullptr;
-  bool busy = false;
+  std::atomic<bool> busy{false};  // taken under the pool mutex, released by its user
 };
 
 struct PaddingPool {
@@ -326,7 +326,7 @@ ta_status padding_slot(size_t n, PaddingSlot** out) {
   std::lock_guard<std::mutex> lock(pool.mu);
   PaddingSlot* pick = nullptr;
   for (auto& sl : pool.slots) {
-    if (sl->busy || sl->cap < n) continue;
+    if (sl->busy.load(std::memory_order_acquire) || sl->cap < n) continue;
     const cudaError_t q = cudaEventQuery(sl->done);
     if (q == cudaSuccess) {
       pick = sl.get();
@@ -350,7 +350,7 @@ ta_status padding_slot(size_t n, PaddingSlot** out) {
     pick = sl.get();
     pool.slots.push_back(std::move(sl));
   }
-  pick->busy = true;
+  pick->busy.store(true, std::memory_order_relaxed);
   *out = pick;
   return TA_OK;
 }
@@ -407,7 +407,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
       cudaError_t e = cudaMemcpyAsync(slot->dev, slot->host, size_t(mask_args.batches) * sizeof(int),
                                       cudaMemcpyHostToDevice, cs);
       if (e != cudaSuccess) {
-        slot->busy = false;
+        slot->busy.store(false, std::memory_order_release);
         return cuda_fail(e, "padding lengths (copy)");
       }
       L.args.valid_len_dev = slot->dev;
@@ -425,7 +425,7 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
   if (slot != nullptr) {
     // the slot is free again once this launch (which read it) completes
     cudaError_t er = cudaEventRecord(slot->done, cs);
-    slot->busy = false;
+    slot->busy.store(false, std::memory_order_release);  // after the record
     if (e == cudaSuccess && er != cudaSuccess) e = er;
   }
   if (e != cudaSuccess) return cuda_fail(e, "sdpa_fwd launch");

@@ -1,0 +1,430 @@
+// D=64 forward: persistent CTAs over (head, query block) work items.
+//
+// Included by sdpa_fwd_sm100.cu inside namespace ta::{anon} (shares Cfg,
+// Roles, the PTX helpers and the softmax constants).  Same algorithm per
+// item as the one-item S/P-rotation kernel (reference item_body,
+// tiled.cpp:144-221): one 128-row Q tile, K/V tiles of 128 keys through a
+// 4-slot TMA ring, S/P rotating through three 64-column TMEM units, stale-max
+// online softmax, O staged in the dead Q buffer and written by TMA.
+//
+// What persistence adds (VERDICT r1 "D=64 and short-S throughput"): a grid of
+// two CTAs per SM walks the work items (item = blockIdx.x + k * gridDim.x),
+// so the per-CTA fixed cost -- barrier init, TMEM allocation, and the ~5700
+// cycles from launch to the first S of a short-sequence item (ViT: 8 K/V
+// tiles per item) -- is paid once per CTA; the next item's Q (double-
+// buffered) and first K/V tiles load while this item's last tiles and
+// epilogue run, and its first QK^T issues as soon as the softmax has read
+// this item's last S.  All per-tile barrier phases and the S/P rotation
+// follow a CTA-global tile counter g, the ring a global position, so items
+// chain without resets:
+//   * S(g) occupies U0U1 (g even) or U1U2 (g odd), P(g) U0 or U2, O U3;
+//     QK(g+1) waits for s_read(g) whichever item g belongs to;
+//   * the Q buffer of the c-th loaded item is c & 1; the TMA thread reloads
+//     it after q_empty (the epilogue's TMA store has read the O staged there);
+//   * o_last completes once per item (the epilogue's wait), o_full / o_half
+//     once per tile (stale-max slow path only).
+// Items with no admitted key (padding valid_len = 0) load nothing and write
+// zeros directly.
+
+struct BarriersD64 {
+  uint64_t q_full[2];
+  uint64_t q_empty[2];
+  uint64_t s_full;
+  uint64_t s_read;
+  uint64_t p_full[2][4];  // [g & 1][P part]
+  uint64_t o_full;
+  uint64_t o_half;
+  uint64_t o_last;
+  uint64_t slot_full[8];
+  uint64_t slot_empty[8];
+  uint32_t tmem_base;
+};
+
+template <bool kBF16, bool kTrace>
+__global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
+    sdpa_d64_persistent_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                               const __grid_constant__ CUtensorMap tmap_k,
+                               const __grid_constant__ CUtensorMap tmap_v,
+                               const __grid_constant__ CUtensorMap tmap_o, FwdArgs args) {
+  constexpr int D = 64;
+  using C = Cfg<D, 1>;
+  using R = Roles<1>;
+  static_assert(C::kRot && !C::kConsumeOrder && C::kRegions == 1, "D=64 rotation layout");
+  constexpr int kTile = C::kTileBytes;  // 16 KB: one Q / K / V tile
+  constexpr int kSlots = C::kSlots;
+  constexpr int kEmu16 = TA_EMU16_D64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sq = smem_u32(smem);         // Q buffers 0, 1
+  const uint32_t sring = sq + 2 * kTile;      // K/V ring
+  BarriersD64* bars = reinterpret_cast<BarriersD64*>(smem + 2 * kTile + kSlots * kTile);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int S = args.seq_len;
+  const int n_qblk = (S + kBM - 1) / kBM;
+  const int n_items = n_qblk * args.bh_count;
+  // per-item geometry (every role derives the same sequence)
+  struct Item {
+    int bh, q0, kv_len, n_kv_seq, n_kv;
+  };
+  auto item_of = [&](int it) {
+    Item I;
+    I.bh = it / n_qblk;
+    const int qin = it - I.bh * n_qblk;
+    const int qblk = args.mask == kMaskCausal ? n_qblk - 1 - qin : qin;  // LPT within a head
+    I.q0 = qblk * kBM;
+    I.kv_len = args.mask != kMaskPadding ? S
+               : args.valid_len_dev != nullptr
+                   ? args.valid_len_dev[(args.bh_offset + I.bh) / args.heads]
+                   : args.valid_len[(args.bh_offset + I.bh) / args.heads];
+    I.n_kv_seq = (I.kv_len + kBN128 - 1) / kBN128;
+    I.n_kv = args.mask == kMaskCausal ? min((I.q0 + kBM - 1) / kBN128 + 1, I.n_kv_seq) : I.n_kv_seq;
+    return I;
+  };
+  long long* const trace = (kTrace && blockIdx.x == 0) ? args.trace : nullptr;
+  auto rec = [&](int ev, int j) {
+    if (trace != nullptr && j < kTraceIters) trace[ev * kTraceIters + j] = clock64();
+  };
+  if (threadIdx.x == 0) rec(kEvKernelStart, 0);
+
+  if (threadIdx.x == R::kWarpTma * 32) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&bars->q_full[b]), 1);
+      mbar_init(smem_u32(&bars->q_empty[b]), 1);
+    }
+    mbar_init(smem_u32(&bars->s_full), 1);
+    mbar_init(smem_u32(&bars->s_read), kBM / 32);
+    for (int b = 0; b < 2; ++b)
+      for (int q = 0; q < kPParts; ++q) mbar_init(smem_u32(&bars->p_full[b][q]), kBM / 32);
+    mbar_init(smem_u32(&bars->o_full), 1);
+    mbar_init(smem_u32(&bars->o_half), 1);
+    mbar_init(smem_u32(&bars->o_last), 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(smem_u32(&bars->slot_full[s]), 1);
+      mbar_init(smem_u32(&bars->slot_empty[s]), 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmap_q);
+    tma_prefetch_desc(&tmap_k);
+    tma_prefetch_desc(&tmap_v);
+  }
+  if (warp == R::kWarpAlloc) tmem_alloc<R::kTmemCols>(smem_u32(&bars->tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+  if (threadIdx.x == 0) rec(kEvKernelStart, 1);
+
+  if (warp >= uint32_t(R::kSoftmaxWarps)) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::kRegsControl));
+    if (warp == R::kWarpTma) {
+      // ------------------------------------------------------------- TMA
+      if (lane == 0) {
+#ifdef TA_D64_STAGGER_NS  // A/B: offset the second co-resident CTA's start
+        if (blockIdx.x >= gridDim.x / 2) __nanosleep(TA_D64_STAGGER_NS);
+#endif
+        uint32_t pos = 0;  // global ring position: K_g at 2g, V_g at 2g + 1
+        int c_load = 0;    // items whose Q was loaded
+        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+          const Item I = item_of(it);
+          if (I.n_kv == 0) continue;
+          const int b = c_load & 1;
+          if (c_load >= 2)  // the epilogue of item c_load - 2 has read its O staging
+            mbar_wait_ctrl(smem_u32(&bars->q_empty[b]), uint32_t(((c_load >> 1) - 1) & 1));
+          const uint32_t qbar = smem_u32(&bars->q_full[b]);
+          mbar_arrive_expect_tx(qbar, kTile);
+          tma_load_3d(sq + b * kTile, &tmap_q, qbar, 0, I.q0, I.bh);
+          for (int p = 0; p < 2 * I.n_kv; ++p, ++pos) {
+            const int slot = int(pos % kSlots);
+            if (pos >= uint32_t(kSlots))
+              mbar_wait_ctrl(smem_u32(&bars->slot_empty[slot]), uint32_t(((pos / kSlots) & 1) ^ 1));
+            const uint32_t fbar = smem_u32(&bars->slot_full[slot]);
+            mbar_arrive_expect_tx(fbar, kTile);
+            tma_load_3d(sring + slot * kTile, (p & 1) ? &tmap_v : &tmap_k, fbar, 0,
+                        (p >> 1) * kBN128, I.bh);
+          }
+          ++c_load;
+        }
+      }
+    } else if (warp == R::kWarpMma) {
+      // ------------------------------------------------------------- MMA
+      constexpr uint32_t idesc_qk = make_idesc_f16(kBF16, kBM, kBN128, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_f16(kBF16, kBM, D, false, true);
+      const uint64_t qdesc = sdesc_sw128(sq, 16, 1024);
+      const uint64_t kdesc = sdesc_sw128(sring, 16, 1024);
+      const uint64_t vdesc = sdesc_sw128(sring, C::kKVRegionBytes, 1024);
+      auto wait_full = [&](uint32_t pos) {
+        mbar_wait_ctrl(smem_u32(&bars->slot_full[pos % kSlots]), uint32_t((pos / kSlots) & 1));
+        tc_fence_after();
+      };
+      auto release = [&](uint32_t pos) {
+        umma_commit_warp(smem_u32(&bars->slot_empty[pos % kSlots]));
+      };
+      auto issue_qk = [&](int b, uint32_t pos, uint32_t g) {  // S(g) = Q K_g^T
+        umma_ss_x4<2, 2>(tmem + C::s_col(int(g)), qdesc + uint64_t((b * kTile) >> 4),
+                         kdesc + uint64_t(((pos % kSlots) * kTile) >> 4), idesc_qk, 0u);
+        umma_commit_warp(smem_u32(&bars->s_full));
+      };
+      auto issue_pv = [&](uint32_t pos, uint32_t g, bool accumulate) {  // O += P(g) V_g
+        const uint32_t tP = tmem + C::p_col(int(g));
+        const uint64_t vd = vdesc + uint64_t(((pos % kSlots) * kTile) >> 4);
+#pragma unroll
+        for (int h = 0; h < kPParts; ++h) {
+          mbar_wait_ctrl(smem_u32(&bars->p_full[g & 1][h]), uint32_t((g >> 1) & 1));
+          tc_fence_after();
+          constexpr int kSteps = kBN128 / 16 / kPParts;
+          static_assert(kSteps % 4 == 0, "P part = 4k K-steps");
+#pragma unroll
+          for (int q = 0; q < kSteps / 4; ++q) {
+            const int ks0 = h * kSteps + q * 4;
+            constexpr int kVStep = (16 * 128) >> 4;  // 16 V rows per K-step
+            umma_ts_x4<kVStep>(tmem + C::kTmemO, tP + ks0 * 8,
+                                        vd + uint64_t((ks0 * 16 * 128) >> 4), idesc_pv,
+                                        (accumulate || ks0 > 0) ? 1u : 0u);
+          }
+          if (h == 0) umma_commit_warp(smem_u32(&bars->o_half));
+        }
+        umma_commit_warp(smem_u32(&bars->o_full));
+      };
+      uint32_t g = 0;    // global K/V tile
+      int c_load = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int n = item_of(it).n_kv;
+        if (n == 0) continue;
+        const int b = c_load & 1;
+        mbar_wait_ctrl(smem_u32(&bars->q_full[b]), uint32_t((c_load >> 1) & 1));
+        tc_fence_after();
+        // S(g) overlaps S(g-1)'s columns: after the softmax has read S(g-1)
+        if (g > 0) {
+          mbar_wait_ctrl(smem_u32(&bars->s_read), uint32_t((g - 1) & 1));
+          tc_fence_after();
+        }
+        wait_full(2 * g);
+        issue_qk(b, 2 * g, g);
+        release(2 * g);
+        for (int j = 0; j < n; ++j) {
+          const uint32_t gj = g + uint32_t(j);
+          if (j + 1 < n) {  // S(g_j + 1) once the softmax holds S(g_j)
+            mbar_wait_ctrl(smem_u32(&bars->s_read), uint32_t(gj & 1));
+            tc_fence_after();
+            wait_full(2 * (gj + 1));
+            issue_qk(b, 2 * (gj + 1), gj + 1);
+            release(2 * (gj + 1));
+          }
+          wait_full(2 * gj + 1);
+          issue_pv(2 * gj + 1, gj, j > 0);
+          release(2 * gj + 1);
+        }
+        umma_commit_warp(smem_u32(&bars->o_last));
+        g += uint32_t(n);
+        ++c_load;
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- softmax
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R::kRegsSoftmax));
+    const uint32_t wq = warp & 3;
+    const int row = int(wq * 32 + lane);
+    const uint32_t lane_off = (wq * 32u) << 16;
+    const uint32_t tS0 = tmem + lane_off;
+    const uint32_t tO = tmem + lane_off + C::kTmemO;
+    const float sl2 = args.scale_log2;
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    const uint32_t sbar = smem_u32(&bars->s_full);
+    const uint32_t obar = smem_u32(&bars->o_full);
+    const int dm = args.head_dim;
+    uint32_t g = 0;
+    int c_load = 0;
+    bool first_item = true;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item I = item_of(it);
+      const int n = I.n_kv;
+      float m_run = -INFINITY;
+      float l_run = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const uint32_t gj = g + uint32_t(j);
+        mbar_wait(sbar, gj & 1);
+        tc_fence_after();
+        const bool tr = kTrace && first_item && row == TA_TRACE_ROW;
+        if (tr) rec(kEvSm0SReady, j);
+        const uint32_t tS = tS0 + C::s_col(int(gj));
+        const uint32_t tP = tS0 + C::p_col(int(gj));
+        uint32_t sr[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
+        tmem_wait_ld();
+        tc_fence_before();  // S(g_j) is in registers: its columns may take S(g_j + 1)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars->s_read));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
+        if (tr) rec(kEvSm0Loaded, j);
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(sr[c][i]);
+        {  // last admitted key of the row in this tile (ragged / padding / causal)
+          int lim = kBN128 - 1;
+          if (j == I.n_kv_seq - 1) lim = min(lim, I.kv_len - j * kBN128 - 1);
+          if (args.mask == kMaskCausal) lim = min(lim, I.q0 + row - j * kBN128);
+          if (lim < kBN128 - 1) {
+#pragma unroll
+            for (int i = 0; i < 128; ++i)
+              if (i > lim) s[i] = -INFINITY;
+          }
+        }
+        if (j == 0) {  // first tile of the item: the exact row max (no O yet)
+          float mx8[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+#pragma unroll
+          for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+          m_run = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+        }
+        float m_use = m_run == -INFINITY ? 0.f : m_run;
+#pragma unroll
+        for (int h = 0; h < kPParts; ++h) {
+          constexpr int kCols = kBN128 / kPParts;
+          uint32_t pk[kCols / 32][16];
+          uint64_t acc[4];
+          auto part_exps = [&]() {
+            const uint64_t negm2 = f2(-m_use, -m_use);
+            acc[0] = acc[1] = acc[2] = acc[3] = 0ull;
+#pragma unroll
+            for (int q = 0; q < kCols / 8; ++q) {
+              const int c0 = h * kCols + q * 8;
+              uint64_t x[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                x[u] = ffma2(f2(s[c0 + 2 * u], s[c0 + 2 * u + 1]), sl2x2, negm2);
+              float p[8];
+              const int emu_pairs = (q & 1) ? kEmu16 / 4 : kEmu16 / 2 - kEmu16 / 4;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (u >= 4 - emu_pairs) {
+                  ex2_poly2(x[u], p[2 * u], p[2 * u + 1]);
+                } else {
+                  float a, bb;
+                  f2_split(x[u], a, bb);
+                  p[2 * u] = ex2(a);
+                  p[2 * u + 1] = ex2(bb);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                acc[u] = fadd2(acc[u], f2(p[2 * u], p[2 * u + 1]));
+                pk[(q * 4 + u) / 16][(q * 4 + u) % 16] = pack2<kBF16>(p[2 * u], p[2 * u + 1]);
+              }
+            }
+          };
+          auto part_sum = [&]() {
+            float lo, hi;
+            f2_split(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), lo, hi);
+            return lo + hi;
+          };
+          part_exps();
+          float psum = part_sum();
+          if (j > 0 && __any_sync(0xffffffffu, !(psum <= kSumGuard))) {
+            // stale-max slow path (as in the one-item kernel): move m to the
+            // part's max, rescale l and O -- after PV(g_j - 1) (part 0) or
+            // PV(g_j) over part 0 (o_half) has landed -- and redo the part
+            float hm4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) hm4[i] = s[h * kCols + i];
+#pragma unroll
+            for (int i = 4; i < kCols; ++i) hm4[i & 3] = fmaxf(hm4[i & 3], s[h * kCols + i]);
+            const float m_part = fmaxf(fmaxf(hm4[0], hm4[1]), fmaxf(hm4[2], hm4[3])) * sl2;
+            const bool need = !(psum <= kSumGuard) && m_part > m_run;
+            const float alpha = need ? ex2(m_run - m_part) : 1.f;
+            if (need) {
+              l_run *= alpha;
+              m_run = m_part;
+              m_use = m_run;
+            }
+            mbar_wait(obar, (gj - 1) & 1);
+            if (h != 0) mbar_wait(smem_u32(&bars->o_half), gj & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < D / 16; ++c) {
+              uint32_t orow[16];
+              tmem_ld16(tO + c * 16, orow);
+              tmem_wait_ld();
+              reg_fence(orow);
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+              tmem_st16(tO + c * 16, orow);
+            }
+            part_exps();
+            psum = part_sum();
+          }
+          l_run += psum;
+#pragma unroll
+          for (int i = 0; i < kCols / 32; ++i) tmem_st16(tP + h * (kCols / 2) + i * 16, pk[i]);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[gj & 1][h]));
+        }
+        if (tr) rec(kEvSm0PArrive, j);
+      }
+
+      // ---------------------------------------------------------- epilogue
+      const int grow = I.q0 + row;
+      const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+      if (n > 0) {
+        mbar_wait(smem_u32(&bars->o_last), uint32_t(c_load & 1));
+        tc_fence_after();
+        const int b = c_load & 1;
+        const uint32_t so = sq + b * kTile;  // this item's (dead) Q buffer
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t orow[32];
+          tmem_ld32(tO + c * 32, orow);
+          tmem_wait_ld();
+          reg_fence(orow);
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            packed[i] = pack2<kBF16>(__uint_as_float(orow[2 * i]) * inv_l,
+                                     __uint_as_float(orow[2 * i + 1]) * inv_l);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t k = uint32_t(c * 4 + i);
+            st_shared_v4(so + row * 128 + ((k ^ (row & 7)) << 4), packed[4 * i],
+                         packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+        tc_fence_before();  // O read before the next item's PV overwrites it
+        fence_proxy_async_smem();
+        named_bar_sync(1, kBM);  // the four softmax warps
+        if (row == 0) {
+          tma_store_3d(&tmap_o, so, 0, I.q0, I.bh);
+          tma_store_commit();
+          tma_store_wait_read0();  // the staging is read: the buffer may take a new Q
+          mbar_arrive(smem_u32(&bars->q_empty[b]));
+        }
+        ++c_load;
+      } else if (grow < S) {  // no admitted key: zeros, written directly
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(args.o) +
+                                              (size_t(I.bh) * S + grow) * dm);
+        for (int i = 0; i < dm / 8; ++i) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      if (args.lse != nullptr && grow < S)
+        args.lse[size_t(I.bh) * S + grow] =
+            l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+      if (kTrace && first_item && row == 0) rec(kEvEpilogueDone, 0);
+      g += uint32_t(n);
+      first_item = false;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == R::kWarpAlloc) tmem_dealloc<R::kTmemCols>(tmem);
+}

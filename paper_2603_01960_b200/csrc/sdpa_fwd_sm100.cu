@@ -461,6 +461,10 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         for (int r = 0; r < C::kRegions; ++r) {  // 4 K-steps of 16 per 128-B swizzle region
           const uint32_t off = (r * C::kRegionBytes) >> 4;      // Q region r
           const uint32_t koff = (r * C::kKRegionBytes) >> 4;  // K region r
+#ifdef TA_DEBUG_NO_MMA  // energy ablation only (wrong results): no tensor-core work
+          if (true) {
+          } else
+#endif
           if constexpr (kPair) {
             umma_ss_x4_pair<2, 2>(dS, qd + off, kd + koff, idesc_qk, r > 0);
           } else if (D <= 128 || n_kstep >= 4 * r + 4) {
@@ -488,6 +492,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           // P columns: 8 per K-step of 16 keys; split softmax: part h (one
           // warp's kBN / 2 keys) over the first kBN / 4 S columns of its half
           const uint32_t tPh = tP + (C::kSplit ? h * (kBN / 2 - kSteps * 8) : 0);
+#ifdef TA_DEBUG_NO_MMA
+          if (false)
+#endif
           if constexpr (kSteps % 4 == 0) {
 #pragma unroll
             for (int g = 0; g < kSteps / 4; ++g) {
@@ -1128,6 +1135,8 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
   }
 }
 
+#include "sdpa_d64_sm100.cuh"
+
 // ----------------------------------------------------------------------------
 // Descriptor self-test: one 128x128x128 UMMA product, checked on the host.
 //   mode 0: D = A * B^T, A [128][128] K-major, B [128 n][128 k] K-major (QK^T)
@@ -1317,6 +1326,44 @@ int fwd_ring_slots(int D, int block_n) {
 
 int fwd_kernel_head_dim(int64_t D) { return D <= 64 ? 64 : D <= 128 ? 128 : D <= 192 ? 192 : 256; }
 
+// D=64: persistent CTAs (two per SM) over the (head, query block) items
+// (sdpa_d64_sm100.cuh); TA_D64_PERSIST=0 keeps the one-item-per-CTA grid
+#ifndef TA_D64_PERSIST
+#define TA_D64_PERSIST 0
+#endif
+
+template <bool kBF16>
+cudaError_t launch_d64_persistent(const FwdLaunch& L) {
+  auto kern = L.args.trace != nullptr ? sdpa_d64_persistent_kernel<kBF16, true>
+                                      : sdpa_d64_persistent_kernel<kBF16, false>;
+  constexpr int kSmem = 2 * Cfg<64, 1>::kTileBytes + Cfg<64, 1>::kSlots * Cfg<64, 1>::kTileBytes +
+                        1024 /*barriers*/ + 1024 /*align pad*/;
+  static_assert(sizeof(BarriersD64) <= 1024, "barrier block");
+  static bool attr_set[64][2] = {};
+  static int sms[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int tr = L.args.trace != nullptr;
+  if (dev < 64 && !attr_set[dev][tr]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev][tr] = true;
+  }
+  if (dev < 64 && sms[dev] == 0) {
+    cudaError_t e = cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t items = int64_t((L.args.seq_len + kBM - 1) / kBM) * L.bh;
+  if (items > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
+  const int64_t slots = int64_t(dev < 64 ? sms[dev] : 148) * Roles<1>::kMinBlocks;
+  const unsigned grid = unsigned(items < slots ? items : slots);
+  FwdArgs a = L.args;
+  a.bh_count = int(L.bh);
+  kern<<<grid, Roles<1>::kThreads, kSmem, static_cast<cudaStream_t>(L.stream)>>>(
+      *L.tmap_q, *L.tmap_k, *L.tmap_v, *L.tmap_o, a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
   if (L.head_dim == 128) {
     if constexpr (kHasBN64) {
@@ -1329,7 +1376,11 @@ cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
     }
     return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
   }
-  if (L.head_dim == 64) return L.bf16 ? launch_typed<64, true>(L) : launch_typed<64, false>(L);
+  if (L.head_dim == 64) {
+    if constexpr (TA_D64_PERSIST != 0 && kQTilesFor<64> == 1 && TA_D64_ROT)
+      return L.bf16 ? launch_d64_persistent<true>(L) : launch_d64_persistent<false>(L);
+    return L.bf16 ? launch_typed<64, true>(L) : launch_typed<64, false>(L);
+  }
   if (L.head_dim == 192) return L.bf16 ? launch_typed<192, true>(L) : launch_typed<192, false>(L);
   if (L.head_dim == 256) return L.bf16 ? launch_typed<256, true>(L) : launch_typed<256, false>(L);
   return cudaErrorInvalidValue;

@@ -27,6 +27,7 @@ struct FwdArgs {
   int mask;          // FwdMask
   int heads;         // H: batch index of flattened head bh is (bh_offset + bh) / H
   int bh_offset;     // first flattened head of this launch (chunked host path)
+  int bh_count;      // flattened heads of this launch (persistent kernels' item count)
   // diagnostics: when non-null, CTA (0,0) records clock64 timestamps
   // trace[event * kTraceIters + j] for the first kTraceIters K/V iterations
   long long* trace;

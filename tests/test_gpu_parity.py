@@ -539,3 +539,41 @@ def test_schedule_selects_executed_block_n(ta, cuda_device, t_n, want):
     q, k, v = O.make_input((1, 1, 300, 64), O.BF16, 3)
     run_gpu_sched(ta, q, k, v, O.BF16, ta.TileSchedule(64, t_n, 2), stats=st)
     assert st.block_n == 128
+
+
+# ---------------------------------- padding lengths beyond the kernel params
+def test_padding_more_than_32_batches_uses_the_pool(ta, cuda_device):
+    # B > 32: valid_len travels through the per-device pinned/device slot pool
+    # (c_api.cpp padding_slot); back-to-back calls on two streams reuse and
+    # grow the pool while earlier launches may still read their slots
+    import torch
+    rng = np.random.default_rng(41)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for trial, B in enumerate((33, 40, 100, 40, 257)):
+        S, H, D = 70, 1, 64
+        q, k, v = O.make_input((B, H, S, D), O.BF16, 9100 + trial)
+        vl = [int(x) for x in rng.integers(0, S + 1, size=B)]
+        qd, kd, vd = (torch.from_numpy(x).bfloat16().cuda() for x in (q, k, v))
+        outs = []
+        for s in streams:
+            with torch.cuda.stream(s):
+                outs.append(ta.sdpa(qd, kd, vd, valid_len=vl, return_lse=True))
+        torch.cuda.synchronize()
+        r = oracle_ref(q, k, v, mask_kind=O.MASK_PADDING, valid_len=vl)
+        for o, lse in outs:
+            assert np.abs(o.double().cpu().numpy() - r["o"]).max() <= TOL[O.BF16], (B, trial)
+            _check_lse(lse.double().cpu().numpy(), r["lse"])
+
+
+def test_release_workspace_then_host_entry_again(ta, cuda_device):
+    import torch
+    q, k, v = O.make_input((1, 2, 300, 64), O.F16, 4)
+    shape = q.shape
+    ht = [torch.from_numpy(x).half() for x in (q, k, v)]
+    for _ in range(2):
+        o = torch.empty(shape, dtype=torch.float16)
+        ta.sdpa_fwd_host(ht[0].data_ptr(), ht[1].data_ptr(), ht[2].data_ptr(), o.data_ptr(), 0,
+                         shape, ta.F16)
+        r = oracle_ref(q, k, v)
+        assert np.abs(o.double().numpy() - r["o"]).max() <= TOL[O.F16]
+        ta.release_workspace(0)
