@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
   constexpr int D = 64;
   using C = Cfg<D, 1>;
   using R = Roles<1>;
-  static_assert(C::kRot && !C::kConsumeOrder && C::kRegions == 1, "D=64 rotation layout");
+  static_assert(C::kRot && C::kRegions == 1, "D=64 rotation layout");  // (plain ring order)
   constexpr int kTile = C::kTileBytes;  // 16 KB: one Q / K / V tile
   constexpr int kSlots = C::kSlots;
   constexpr int kEmu16 = TA_EMU16_D64;

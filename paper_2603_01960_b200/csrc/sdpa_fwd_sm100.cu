@@ -66,8 +66,12 @@ struct Roles {
   // CTAs: 32768/256 -> 128, 128*(200-128) == 128*(128-56)).
   static constexpr int kLaunchRegs = kWide ? 248 : (65536 / (kThreads * kMinBlocks)) & ~7;
   // (kSplit: 640 threads -> 96; 512 * (104 - 96) <= 128 * (96 - 56))
-  static constexpr int kRegsSoftmax = kWide ? 248 : kSplit ? 104 : kQT == 1 ? 200 : 208;
-  static constexpr int kRegsControl = kWide ? 248 : kSplit ? 56 : kQT == 1 ? 56 : 88;
+#ifndef TA_QT1_REGS_SOFTMAX  // register split at QT=1 (two CTAs per SM), A/B knob
+#define TA_QT1_REGS_SOFTMAX 200
+#endif
+  static constexpr int kRegsSoftmax = kWide ? 248 : kSplit ? 104 : kQT == 1 ? TA_QT1_REGS_SOFTMAX : 208;
+  static constexpr int kRegsControl =
+      kWide ? 248 : kSplit ? 56 : kQT == 1 ? 256 - TA_QT1_REGS_SOFTMAX : 88;
   static_assert(kSoftmaxWarps * 32 * (kRegsSoftmax - kLaunchRegs) <=
                     (kThreads - kSoftmaxWarps * 32) * (kLaunchRegs - kRegsControl),
                 "setmaxnreg.inc would wait forever: register pool does not balance");
@@ -185,7 +189,10 @@ struct Cfg {
   // with the 2-3 slot rings of D > 128 the next K no longer waits behind a V
   // slot that frees only when PV completes (+32-36% at D=160/256; D=64 with
   // 4 slots gains nothing and keeps the plain order)
-  static constexpr bool kConsumeOrder = kRot && D > 128;
+#ifndef TA_D64_CONSUME
+#define TA_D64_CONSUME 0
+#endif
+  static constexpr bool kConsumeOrder = kRot && (D > 128 || TA_D64_CONSUME);
   static constexpr uint32_t kTmemS = 0;                  // S_t at col 128 t (fp32)
   static constexpr uint32_t kTmemO = kRot ? 192 : 128 * kQT;  // O_t at kTmemO + D t (fp32)
   __device__ static constexpr uint32_t s_col(int j) { return kRot ? 64u * uint32_t(j & 1) : 0u; }
@@ -404,6 +411,16 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
     }
   } else if (warp == kWarpTrace) {
     // optional tracer: timestamps of tensor-core completions (diagnostics only)
+    if (kTrace && C::kRot && lane == 0 && trace != nullptr) {  // S(j+1), then PV(j)
+      for (int j = 0; j < n_kv && j < kTraceIters; ++j) {
+        if (j + 1 < n_kv) {
+          mbar_wait(smem_u32(&bars->s_full[0]), uint32_t((j + 1) & 1));
+          rec(kEvTcS0Done, j);
+        }
+        mbar_wait(smem_u32(&bars->o_full[0]), uint32_t(j & 1));
+        rec(kEvTcPV0Done, j);
+      }
+    }
     if (kTrace && kQT == 2 && lane == 0 && trace != nullptr) {
       for (int j = 0; j < n_kv && j < kTraceIters; ++j) {
         mbar_wait(smem_u32(&bars->o_full[0]), uint32_t(j & 1));
@@ -542,8 +559,11 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
               if constexpr (C::kConsumeOrder) rk = 2 * j + 1;
               mbar_wait_ctrl(smem_u32(&bars->s_read), uint32_t(j & 1));
               tc_fence_after();
+              if (lane == 0) rec(kEvMmaWaitP1, j);  // (rotation traces: s_read(j) seen)
               wait_full(rk);
+              if (lane == 0) rec(kEvMmaIssuedPV1, j);  // (... K_{j+1} landed)
               issue_qk(0, rk, C::s_col(j + 1));
+              if (lane == 0) rec(kEvSm1PArrive, j);  // (... QK(j+1) issued)
               release(rk);
             }
             int rv = 2 * j + 1;  // V_j
@@ -862,6 +882,8 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
       tc_fence_after();
       const bool tr = kTrace && row == TA_TRACE_ROW;
       if (tr) rec(kEvSm0SReady + 5 * t, j);
+      // (one-tile rotation traces: S ready / loaded as seen by warps 1..3)
+      if (kTrace && C::kRot && wq > 0 && lane == 0) rec(kEvSm1SReady + int(wq) - 1, j);
       const uint32_t tS = tS0 + C::s_col(j);  // S(j)
       const uint32_t tP = tS0 + C::p_col(j);  // P(j)
       uint32_t sr[4][32];
@@ -876,6 +898,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
 #pragma unroll
       for (int c = 0; c < 4; ++c) reg_fence(sr[c]);
       if (tr) rec(kEvSm0Loaded + 5 * t, j);
+      if (kTrace && C::kRot && wq == 3 && lane == 0) rec(kEvSm1Exp, j);  // (warp 3 loaded)
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
