@@ -127,6 +127,7 @@ constexpr int kPParts = TA_P_PARTS;
 #endif
 constexpr bool kStaleMax = TA_STALE_MAX != 0;
 constexpr float kSumGuard = 256.0f;
+
 // every completed mbarrier phase is waited on by some thread (the slow-path
 // barriers o_full / o_half included), so compute-sanitizer synccheck sees no
 // unobserved phase
@@ -870,6 +871,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
 
     const int my_n_kv = n_kv_t[t];
     for (int j = 0; j < my_n_kv; ++j) {
+      // (rotation traces: warp 0 about to wait for S(j); j = 0 is overwritten
+      // by the row-max stamp below)
+      if (kTrace && C::kRot && row == TA_TRACE_ROW) rec(kEvSm0Max + 5 * t, j);
       mbar_wait(sbar, uint32_t(j & 1));
       // observe PV(j-1)'s o_full / o_half phases (synccheck "missing wait"):
       // without the rotation S(j) follows PV(j-1) in issue order, so both are
