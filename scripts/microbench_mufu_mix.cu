@@ -5,6 +5,9 @@
 //   mode 2: mode 1 + F2FP pack of each pair
 //   mode 3: mode 2 + FADD2 row-sum accumulation (4 chains)
 //   mode 4: mode 2 with the FFMA2s of the whole row issued first
+//   mode 5: FFMA2 -> F2FP (x to bf16x2) -> packed ex2.approx.ftz.bf16x2
+//   mode 6: FFMA2 -> F2FP (x to f16x2) -> packed ex2.approx.f16x2
+//   (cycles are per element exp in every mode)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2603_01960_b200/csrc \
 //        -o /tmp/mbm scripts/microbench_mufu_mix.cu && /tmp/mbm
 #include <cstdio>
@@ -25,6 +28,21 @@ __device__ __forceinline__ uint64_t vffma2(uint64_t a, uint64_t b, uint64_t c) {
 __device__ __forceinline__ uint32_t vpack(float lo, float hi) {
   uint32_t r;
   asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t vex2_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t vex2_f16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t vpack_f16(float lo, float hi) {
+  uint32_t r;
+  asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
 __device__ __forceinline__ uint64_t vfadd2(uint64_t a, uint64_t b) {
@@ -56,6 +74,13 @@ __global__ void __launch_bounds__(512, 1) bench(const float* in, long long* cycl
         f2_split(x[u], a, b);
         const float p0 = vex2(a), p1 = vex2(b);
         acc_pk ^= vpack(p0, p1);
+      }
+    } else if constexpr (MODE == 5 || MODE == 6) {
+#pragma unroll
+      for (int u = 0; u < 64; ++u) {
+        float a, b;
+        f2_split(vffma2(f2(s[2 * u], s[2 * u + 1]), sl2x2, negm2), a, b);
+        acc_pk ^= MODE == 5 ? vex2_bf16x2(vpack(a, b)) : vex2_f16x2(vpack_f16(a, b));
       }
     } else {
 #pragma unroll
@@ -116,6 +141,8 @@ int main() {
     run<2>("FFMA2 -> ex2 pair -> F2FP", w, in, cyc, sink);
     run<3>("... + FADD2 row sum", w, in, cyc, sink);
     run<4>("all FFMA2 first, then ex2 + F2FP", w, in, cyc, sink);
+    run<5>("FFMA2 -> F2FP -> ex2.bf16x2 (per elem)", w, in, cyc, sink);
+    run<6>("FFMA2 -> F2FP -> ex2.f16x2 (per elem)", w, in, cyc, sink);
   }
   return 0;
 }
