@@ -16,6 +16,13 @@
 //     TMEM is rare (tiled.hpp:212 skips the rescale only when alpha == 1);
 //   * LSE = m + ln(l) is emitted as a second output (the reference computes
 //     m and l but never returns them, tiled.hpp:223-238).
+// Instantiations (launch_sdpa_fwd): D=128 two-tile ping-pong with 128-key
+// tiles (the product path) or 64-key tiles (TileSchedule t_n <= 64, split
+// softmax: two warps per row); D=64 and D > 128 one Q tile per CTA with the
+// S/P rotation.  Build options kept for A/B:
+// TA_D128_SPLIT (split softmax at 128 keys), TA_PAIR (cta_group::2 pair),
+// TA_D64_PERSIST (persistent D=64, sdpa_d64_sm100.cuh), TA_OBSERVE_PHASES
+// (synccheck build); TA_DEBUG_* are ablations with wrong results.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
