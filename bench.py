@@ -475,10 +475,11 @@ def run_ours(args):
                               "block_m": stats.block_m, "block_n": stats.block_n,
                               "stages": stats.stages, "q_tiles_per_cta": stats.q_tiles_per_cta,
                               "per_launch_ms": [round(x, 4) for x in per_step]}
-        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:  # last, after NCCL's teardown messages: the output's final line
+        print(json.dumps(line), flush=True)
     return 0
 
 
