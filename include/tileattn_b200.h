@@ -95,6 +95,8 @@ typedef struct ta_kernel_stats {
  *             tiled.hpp:223-238, tiled.cpp:216-220)
  *   lse     : device, [B,H,S] fp32 natural-log log-sum-exp of the scaled
  *             scores (m + ln l); -inf for rows with no admitted key; NULL = skip
+ *             (a NaN input propagates to the O and LSE of the rows whose
+ *             scores it reaches, as the reference's arithmetic does)
  *   valid_len : HOST array of B entries, MaskKind::Padding only (else NULL);
  *             B <= 32 travels in the kernel parameters, larger B through a
  *             per-device pool of pinned/device slots (allocated on first

@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
 
       // ---------------------------------------------------------- epilogue
       const int grow = I.q0 + row;
-      const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+      const float inv_l = l_run != 0.f ? 1.f / l_run : 0.f;  // finalize: l == 0 -> zeros (NaN propagates)
       if (n > 0) {
         mbar_wait(smem_u32(&bars->o_last), uint32_t(c_load & 1));
         tc_fence_after();
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
       }
       if (args.lse != nullptr && grow < S)
         args.lse[size_t(I.bh) * S + grow] =
-            l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+            l_run != 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
       if (kTrace && first_item && row == 0) rec(kEvEpilogueDone, 0);
       g += uint32_t(n);
       first_item = false;

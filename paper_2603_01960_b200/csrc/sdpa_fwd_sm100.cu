@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
     named_bar_sync(pair_bar, 64);
     const float l_tot = l_run + xch[kXL + ((t * 4 + int(wq)) * 2 + (c ^ 1)) * 32 + lane];
     const int grow = q0 + t * kBM + row;
-    const float inv_l = l_tot > 0.f ? 1.f / l_tot : 0.f;
+    const float inv_l = l_tot != 0.f ? 1.f / l_tot : 0.f;  // finalize: l == 0 -> zeros (NaN propagates)
     const int dm = args.head_dim;
     const uint32_t so = sq + t * C::kTileBytes;  // the tile's (dead) Q buffer
 #pragma unroll
@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
     }
     if (c == 0 && args.lse != nullptr && grow < S)
       args.lse[size_t(bh) * S + grow] =
-          l_tot > 0.f ? (m_run + __log2f(l_tot)) * kLn2 : -INFINITY;
+          l_tot != 0.f ? (m_run + __log2f(l_tot)) * kLn2 : -INFINITY;
     if (row == 0 && c == 0) tma_store_wait_read0();
     if (kTrace && row == 0 && c == 0) rec(kEvEpilogueDone, t);
   } else {
@@ -1105,7 +1105,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
       tc_fence_after();
     }
     const int grow = q0 + t * kBM + row;
-    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+    const float inv_l = l_run != 0.f ? 1.f / l_run : 0.f;  // finalize: l == 0 -> zeros (NaN propagates)
     const int dm = args.head_dim;  // stored columns (<= D)
     uint16_t* orow_g = reinterpret_cast<uint16_t*>(args.o) + (size_t(bh) * S + grow) * dm;
     // TMA-store epilogue: the tile's rows go to its (now dead) Q buffer in the
@@ -1155,7 +1155,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
     }
     if (args.lse != nullptr && grow < S)
       args.lse[size_t(bh) * S + grow] =
-          l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+          l_run != 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
     if (kTmaStoreO && row == 0) tma_store_wait_read0();  // smem stays valid until read
     if (kTrace && row == 0) rec(kEvEpilogueDone, t);
   }

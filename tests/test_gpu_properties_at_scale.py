@@ -124,3 +124,29 @@ def test_padding_extremes_at_16k(ta, cuda_device):
                 want = torch.softmax(s, 0) @ vh
                 assert (o[b, h, i].double() - want).abs().max().item() <= 2e-2, (b, h, i)
                 assert abs(lse[b, h, i].item() - torch.logsumexp(s, 0).item()) <= 1e-3
+
+
+def test_nan_propagates_like_the_reference(ta, cuda_device):
+    # a NaN in one query row poisons that row only (its scores are NaN, the
+    # reference's exp / sum propagate it); a NaN key poisons every row whose
+    # mask admits it -- and with causal masking only the rows at or after it
+    import torch
+    B, H, S, D = 1, 2, 1000, 64
+    g = torch.Generator(device="cuda").manual_seed(19)
+    q, k, v = (torch.randn(B, H, S, D, device="cuda", generator=g).half() for _ in range(3))
+    qn = q.clone()
+    qn[0, 0, 123, 5] = float("nan")
+    o, lse = ta.sdpa(qn, k, v, return_lse=True)
+    torch.cuda.synchronize()
+    bad = torch.zeros(S, dtype=torch.bool, device="cuda")
+    bad[123] = True
+    assert bool(torch.isnan(o[0, 0, 123]).all()) and bool(torch.isnan(lse[0, 0, 123]))
+    assert bool(torch.isfinite(o[0, 0, ~bad]).all()) and bool(torch.isfinite(o[0, 1]).all())
+    ref = ta.sdpa(q, k, v)
+    assert torch.equal(o[0, 0, ~bad], ref[0, 0, ~bad])  # other rows untouched, bit for bit
+    kn = k.clone()
+    kn[0, 1, 700, 0] = float("nan")
+    o2 = ta.sdpa(q, kn, v, causal=True)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(o2[0, 1, :700]).all())
+    assert bool(torch.isnan(o2[0, 1, 700:]).any(dim=-1).all())
