@@ -96,7 +96,11 @@ typedef struct ta_kernel_stats {
  *   lse     : device, [B,H,S] fp32 natural-log log-sum-exp of the scaled
  *             scores (m + ln l); -inf for rows with no admitted key; NULL = skip
  *             (a NaN input propagates to the O and LSE of the rows whose
- *             scores it reaches, as the reference's arithmetic does)
+ *             scores it reaches, as the reference's arithmetic does; padded
+ *             K/V rows (>= valid_len) never contribute, like the reference's
+ *             zero-weight skip; one divergence: under the causal mask a NaN /
+ *             inf in V at key k also reaches the rows of k's 128-key tile that
+ *             precede k -- P V on the tensor core multiplies it by weight 0)
  *   valid_len : HOST array of B entries, MaskKind::Padding only (else NULL);
  *             B <= 32 travels in the kernel parameters, larger B through a
  *             per-device pool of pinned/device slots (allocated on first

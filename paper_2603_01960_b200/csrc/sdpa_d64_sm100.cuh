@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
       uint32_t g = 0;    // global K/V tile
       int c_load = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int n = item_of(it).n_kv;
+        const Item I = item_of(it);
+        const int n = I.n_kv;
         if (n == 0) continue;
         const int b = c_load & 1;
         mbar_wait_ctrl(smem_u32(&bars->q_full[b]), uint32_t((c_load >> 1) & 1));
@@ -214,6 +215,15 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
             release(2 * (gj + 1));
           }
           wait_full(2 * gj + 1);
+          if (args.mask == kMaskPadding && j == I.n_kv_seq - 1 && I.kv_len - j * kBN128 < kBN128) {
+            // keys >= valid_len in the last tile get weight 0 (the reference
+            // skips them): zero their V rows so a NaN / inf there cannot reach O
+            const uint32_t vbase = sring + ((2 * gj + 1) % kSlots) * kTile;
+            for (int i = (I.kv_len - j * kBN128) * 8 + int(lane); i < kBN128 * 8; i += 32)
+              st_shared_v4(vbase + (i >> 3) * 128 + (i & 7) * 16, 0u, 0u, 0u, 0u);
+            fence_proxy_async_smem();
+            __syncwarp();
+          }
           issue_pv(2 * gj + 1, gj, j > 0);
           release(2 * gj + 1);
         }

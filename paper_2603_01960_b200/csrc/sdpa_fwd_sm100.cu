@@ -503,6 +503,25 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
       };
       // PV in two halves of 64 keys, each issued as soon as the softmax
       // warpgroup has written that half of P (P aliases S in TMEM).
+      // Padding: keys >= valid_len inside the last K/V tile are real memory
+      // (not TMA zero-fill) and get weight 0; the reference skips zero
+      // weights (online_update, tiled.hpp:215-216), so a NaN / inf there
+      // must not reach O: the MMA warp zeroes those V rows (whole 128-B
+      // swizzle rows) before the tile's first PV reads the slot.
+      auto zero_v_tail = [&](int r, int j) {
+        if (args.mask != kMaskPadding || j != n_kv_seq - 1) return;
+        const int r0 = kv_len - j * kBN;  // first masked key row of the tile
+        if (r0 >= kBN) return;
+        constexpr int kVRegions = kPair ? 1 : C::kRegions;
+        const uint32_t vbase = sring + slot_of(r) * C::kKVBytes;
+        for (int i = r0 * 8 + int(lane); i < kBN * 8; i += 32) {  // 16-B pieces
+          for (int g = 0; g < kVRegions; ++g)
+            st_shared_v4(vbase + g * C::kKVRegionBytes + (i >> 3) * 128 + (i & 7) * 16, 0u, 0u,
+                         0u, 0u);
+        }
+        fence_proxy_async_smem();  // generic-proxy writes before the tensor core reads
+        __syncwarp();
+      };
       auto issue_pv = [&](int t, int r, bool accumulate, int j) {
         const uint32_t tP = tmem + C::kTmemS + t * kBN + C::p_col(j);
         uint64_t vd = kvdesc_v + uint64_t((slot_of(r) * C::kKVBytes) >> 4);
@@ -577,6 +596,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
             int rv = 2 * j + 1;  // V_j
             if constexpr (C::kConsumeOrder) rv = j + 1 < n ? 2 * j + 2 : 2 * n - 1;
             wait_full(rv);
+            zero_v_tail(rv, j);
             issue_pv(0, rv, j > 0, j);
             release(rv);
           }
@@ -597,6 +617,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
             // after it on the tensor pipe
             const int rk = 2 * j, rv = 2 * j - 1;
             wait_full(rv);
+            zero_v_tail(rv, j - 1);
             issue_pv(0, rv, j > 1, j - 1);
             release(rv);
             wait_full(rk);
@@ -605,6 +626,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           }
           const int rv = 2 * n - 1;
           wait_full(rv);
+          zero_v_tail(rv, n - 1);
           issue_pv(0, rv, n > 1, n - 1);
           release(rv);
         }
@@ -621,6 +643,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         for (int j = 1; j < n1; ++j) {
           const int rk = 2 * j, rv = 2 * j - 1;
           wait_full(rv);
+          zero_v_tail(rv, j - 1);
           if (j - 1 < n0) issue_pv(0, rv, j > 1, j - 1);
           wait_full(rk);
           if (j < n0) issue_qk(0, rk);
@@ -631,6 +654,7 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         }
         const int rv = 2 * n1 - 1;
         wait_full(rv);
+        zero_v_tail(rv, n1 - 1);
         if (n1 - 1 < n0) issue_pv(0, rv, n1 > 1, n1 - 1);
         issue_pv(1, rv, n1 > 1, n1 - 1);
         release(rv);

@@ -150,3 +150,27 @@ def test_nan_propagates_like_the_reference(ta, cuda_device):
     torch.cuda.synchronize()
     assert bool(torch.isfinite(o2[0, 1, :700]).all())
     assert bool(torch.isnan(o2[0, 1, 700:]).any(dim=-1).all())
+
+
+@pytest.mark.parametrize("D,t_n", [(64, 128), (128, 128), (128, 64), (160, 128), (256, 128)])
+def test_padding_ignores_nan_beyond_valid_len(ta, cuda_device, D, t_n):
+    # keys >= valid_len have weight 0, and the reference skips zero weights
+    # (online_update, tiled.hpp:215-216): NaN / inf in the padded K and V
+    # rows must not reach O or LSE -- the result equals the clean inputs', bit
+    # for bit, on every kernel (rotation, two-tile, 64-key, wide)
+    import torch
+    B, H, S = 3, 2, 700
+    g = torch.Generator(device="cuda").manual_seed(23 + D)
+    q, k, v = (torch.randn(B, H, S, D, device="cuda", generator=g).bfloat16() for _ in range(3))
+    vl = [300, 129, 700]
+    sched = ta.TileSchedule(64, t_n, 2)
+    o1, l1 = ta.sdpa(q, k, v, valid_len=vl, return_lse=True, schedule=sched)
+    kg, vg = k.clone(), v.clone()
+    for b, n in enumerate(vl):
+        kg[b, :, n:] = float("nan")
+        vg[b, :, n:] = float("inf")
+        vg[b, :, n + 1:n + 3] = float("nan")
+    o2, l2 = ta.sdpa(q, kg, vg, valid_len=vl, return_lse=True, schedule=sched)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    assert bool(torch.isfinite(o2).all())
