@@ -799,18 +799,25 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           m_run = m_new;
           m_use = m_run;
         }
-        mbar_wait(obar, uint32_t((j - 1) & 1));
-        tc_fence_after();
+        // the row's whole O is rescaled by its c = 0 warp: PV(j) over the first
+        // key half -- issued once the four c = 0 warps have handed off P --
+        // accumulates into every O column, so a c = 1 warp still rescaling
+        // its half would race with it
+        if (c == 0) {
+          mbar_wait(obar, uint32_t((j - 1) & 1));
+          tc_fence_after();
+          const uint32_t tOrow = tO - (D / 2) * c;  // (c == 0: the tile's O columns)
 #pragma unroll 1
-        for (int cc = 0; cc < D / 2; cc += 16) {
-          uint32_t orow[16];
-          tmem_ld16(tO + cc, orow);
-          tmem_wait_ld();
-          reg_fence(orow);
+          for (int cc = 0; cc < D; cc += 16) {
+            uint32_t orow[16];
+            tmem_ld16(tOrow + cc, orow);
+            tmem_wait_ld();
+            reg_fence(orow);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
-          tmem_st16(tO + cc, orow);
+            for (int i = 0; i < 16; ++i)
+              orow[i] = __float_as_uint(__uint_as_float(orow[i]) * alpha);
+            tmem_st16(tOrow + cc, orow);
+          }
         }
         psum = exps(sv, m_use, pk);
       }
