@@ -346,8 +346,8 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
 #pragma unroll
             for (int i = 0; i < 4; ++i) hm4[i] = s[h * kCols + i];
 #pragma unroll
-            for (int i = 4; i < kCols; ++i) hm4[i & 3] = fmaxf(hm4[i & 3], s[h * kCols + i]);
-            const float m_part = fmaxf(fmaxf(hm4[0], hm4[1]), fmaxf(hm4[2], hm4[3])) * sl2;
+            for (int i = 4; i < kCols; ++i) hm4[i & 3] = fmax_nan(hm4[i & 3], s[h * kCols + i]);
+            const float m_part = fmax_nan(fmax_nan(hm4[0], hm4[1]), fmax_nan(hm4[2], hm4[3])) * sl2;
             const bool need = !(psum <= kSumGuard) && m_part > m_run;
             const float alpha = need ? ex2(m_run - m_part) : 1.f;
             if (need) {
@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
             }
             part_exps();
             psum = part_sum();
+            if (m_part != m_part) psum = __int_as_float(0x7fffffff);  // NaN score -> NaN row
           }
           l_run += psum;
 #pragma unroll

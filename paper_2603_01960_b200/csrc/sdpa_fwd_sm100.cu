@@ -699,6 +699,11 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
       named_bar_sync(pair_bar, 64);
       return fmaxf(v, *xm_other);
     };
+    auto pair_max_nan = [&](float v) {  // (slow path: a NaN half poisons the row)
+      *xm_mine = v;
+      named_bar_sync(pair_bar, 64);
+      return fmax_nan(v, *xm_other);
+    };
     constexpr int kEmu = kEmu16;
     float m_run = -INFINITY;  // shared by the row's two warps (scaled, log2 units)
     float l_run = 0.f;        // this warp's partial normaliser over its columns
@@ -790,8 +795,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
 #pragma unroll
         for (int i = 0; i < 4; ++i) mx4[i] = sv[i];
 #pragma unroll
-        for (int i = 4; i < kHalf; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], sv[i]);
-        const float m_new = pair_max(fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]))) * sl2;
+        for (int i = 4; i < kHalf; ++i) mx4[i & 3] = fmax_nan(mx4[i & 3], sv[i]);
+        const float m_new =
+            pair_max_nan(fmax_nan(fmax_nan(mx4[0], mx4[1]), fmax_nan(mx4[2], mx4[3]))) * sl2;
         const bool need = m_new > m_run;
         const float alpha = need ? ex2(m_run - m_new) : 1.f;
         if (need) {
@@ -820,6 +826,11 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           }
         }
         psum = exps(sv, m_use, pk);
+        // a NaN score (NaN in q or k) reaches this path on every row it hits
+        // (MUFU gives NaN, the FMA-pipe emulation saturates at 2^127); the
+        // NaN-propagating max above carries it into m_new: make the row's l
+        // NaN so its O and LSE are NaN, as the reference's are
+        if (kEmu > 0 && m_new != m_new) psum = __int_as_float(0x7fffffff);
       }
       l_run += psum;
       // observe o_full's phase j-1 (PV(j-1)) before P(j) lets PV(j) complete
@@ -1065,8 +1076,8 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
 #pragma unroll
           for (int i = 0; i < 4; ++i) hm4[i] = s[h * kCols + i];
 #pragma unroll
-          for (int i = 4; i < kCols; ++i) hm4[i & 3] = fmaxf(hm4[i & 3], s[h * kCols + i]);
-          const float m_part = fmaxf(fmaxf(hm4[0], hm4[1]), fmaxf(hm4[2], hm4[3])) * sl2;
+          for (int i = 4; i < kCols; ++i) hm4[i & 3] = fmax_nan(hm4[i & 3], s[h * kCols + i]);
+          const float m_part = fmax_nan(fmax_nan(hm4[0], hm4[1]), fmax_nan(hm4[2], hm4[3])) * sl2;
           const bool need = !(psum <= kSumGuard) && m_part > m_run;
           const float alpha = need ? ex2(m_run - m_part) : 1.f;
           if (need) {
@@ -1096,6 +1107,10 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           float lo, hi;
           f2_split(fadd2(a01, a23), lo, hi);
           psum = lo + hi;
+          // a NaN score reaches this path on every row it hits (MUFU gives
+          // NaN, the FMA-pipe emulation saturates at 2^127); the NaN-
+          // propagating part max carries it: l NaN -> O, LSE NaN
+          if (kEmu16 > 0 && m_part != m_part) psum = __int_as_float(0x7fffffff);
         }
         l_run += psum;
 #pragma unroll

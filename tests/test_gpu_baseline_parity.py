@@ -155,6 +155,18 @@ def test_exp2_emulation_kat_against_reference_fast_expf(ta, cuda_device):
         assert np.abs(y[~big]).max(initial=0.0) <= 1e-30
         _record(config="exp2_kat", mode=["ex2_poly2", "mufu_ex2"][mode],
                 n=int(x.size), max_rel=float(relerr.max()), tol=rel)
+    # far above the softmax's range (a stale running max): the emulation
+    # saturates at ~2^127 like MUFU's inf, never wraps into garbage; NaN also
+    # saturates (>= 2^127), which trips the softmax's slow-path guard, whose
+    # redo runs on MUFU and yields the NaN (test_nan_in_any_key_column)
+    xs = torch.tensor([9.0, 126.5, 200.0, 1e4, float("inf"), float("nan")], device="cuda")
+    ys = torch.empty_like(xs)
+    rc = ta.lib().ta_debug_exp2(xs.data_ptr(), ys.data_ptr(), xs.numel(), 0,
+                                torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    y = ys.cpu().tolist()
+    assert abs(y[0] / 512.0 - 1.0) <= 1.3e-4
+    assert all(v >= 1e38 or math.isnan(v) for v in y[1:6]), y
     # exact anchor points: 2^0 = 1 and integer powers are exact on both units
     xi = torch.tensor([0.0, -1.0, -2.0, -10.0, -126.0, 1.0, 7.0], device="cuda")
     for mode in (0, 1):

@@ -174,3 +174,60 @@ def test_padding_ignores_nan_beyond_valid_len(ta, cuda_device, D, t_n):
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
     assert bool(torch.isfinite(o2).all())
+
+
+def test_very_long_sequence_sampled_rows(ta, cuda_device):
+    # S = 2^17 (1024 K/V tiles per row, 4x the bench length): sampled rows of
+    # every 256-row CTA class against float64
+    import torch
+    B, H, S, D = 1, 1, 131072, 128
+    g = torch.Generator(device="cuda").manual_seed(29)
+    q, k, v = (torch.randn(B, H, S, D, device="cuda", generator=g).bfloat16() for _ in range(3))
+    o, lse = ta.sdpa(q, k, v, return_lse=True)
+    torch.cuda.synchronize()
+    kd, vd = k[0, 0].double(), v[0, 0].double()
+    for i in (0, 1, 255, 256, 65535, 99999, S - 1):
+        s = (q[0, 0, i].double() @ kd.T) / math.sqrt(D)
+        want = torch.softmax(s, 0) @ vd
+        assert (o[0, 0, i].double() - want).abs().max().item() <= 2e-2, i
+        assert abs(lse[0, 0, i].item() - torch.logsumexp(s, 0).item()) <= 1e-3, i
+
+
+@pytest.mark.parametrize("D", [64, 128, 256])
+def test_extreme_scale_is_one_hot(ta, cuda_device, D):
+    # scale 100: every row's softmax is (numerically) one-hot, the running max
+    # jumps on many tiles (stale-max slow path), and exps of the other keys
+    # underflow to exact 0 -- O must be the argmax key's V row
+    import torch
+    B, H, S = 1, 2, 3000
+    g = torch.Generator(device="cuda").manual_seed(31 + D)
+    q, k, v = (torch.randn(B, H, S, D, device="cuda", generator=g).half() for _ in range(3))
+    o, lse = ta.sdpa(q, k, v, scale=100.0, return_lse=True)
+    torch.cuda.synchronize()
+    s = torch.einsum("bhqd,bhkd->bhqk", q.double(), k.double()) * 100.0
+    top2 = s.topk(2, dim=-1).values
+    clear = (top2[..., 0] - top2[..., 1]) > 1.0  # rows whose max is unambiguous
+    want = torch.softmax(s, -1) @ v.double()
+    err = (o.double() - want).abs().amax(-1)
+    assert bool((err[clear] <= 5e-3).all()), err[clear].max().item()
+    # LSE ~ 6000 here: fp32 carries it to ~5e-7 relative (scores from the fp32
+    # tensor-core sums times scale * log2 e in fp32)
+    want_lse = torch.logsumexp(s, -1)
+    assert bool(((lse.double() - want_lse).abs() <= 2e-3 + 2e-6 * want_lse.abs()).all())
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_nan_in_any_key_column(ta, cuda_device, D):
+    # a NaN key at every column position of a 128-key tile (some land on the
+    # FMA-pipe exp emulation at D=64): every query row admits it, so every
+    # row's O and LSE are NaN, as the reference's arithmetic gives
+    import torch
+    B, H, S = 1, 1, 256
+    for col in range(0, 128, 3):
+        g = torch.Generator(device="cuda").manual_seed(37 + col)
+        q, k, v = (torch.randn(B, H, S, D, device="cuda", generator=g).half() for _ in range(3))
+        k[0, 0, 128 + col, 0] = float("nan")
+        o, lse = ta.sdpa(q, k, v, return_lse=True)
+        torch.cuda.synchronize()
+        assert bool(torch.isnan(lse).all()), col
+        assert bool(torch.isnan(o).any(dim=-1).all()), col
