@@ -319,6 +319,13 @@ def run_ours(args):
         dev = torch.device("cpu")
         if world > 1:
             dist.init_process_group("gloo", rank=rank, world_size=world)
+    elif args.share_device:
+        # GPU test mode: every rank on cuda:0 (gloo), exercising the
+        # multi-rank GPU flow on a one-GPU box; not a scaling measurement
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        if world > 1:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
     else:
         torch.cuda.set_device(local)
         dev = torch.device("cuda", local)
@@ -329,6 +336,7 @@ def run_ours(args):
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
 
+    red_dev = torch.device("cpu") if (stub or args.share_device) else dev  # (gloo: host tensors)
     from paper_2603_01960_b200.sharding import head_range, max_over_ranks
     B, H, S, D = WORKLOAD["B"], WORKLOAD["H"], WORKLOAD["S"], WORKLOAD["D"]
     h0, h1 = head_range(H, world, rank)  # head sharding: this rank owns heads [h0, h1)
@@ -375,8 +383,8 @@ def run_ours(args):
         if sampler:
             sampler.__exit__(None, None, None)
     if world > 1:
-        total_ms = max_over_ranks(total_ms, device=dev)
-        per_step = [max_over_ranks(x, device=dev) for x in per_step]
+        total_ms = max_over_ranks(total_ms, device=red_dev)
+        per_step = [max_over_ranks(x, device=red_dev) for x in per_step]
     ms_step = total_ms / args.steps
     value = job_flops / (ms_step / 1e3) / 1e12
     med, p95 = quantiles(per_step)
@@ -424,7 +432,7 @@ def run_ours(args):
         barrier()
         e2e_s = (time.perf_counter() - t0) / n_e2e
         if world > 1:
-            e2e_s = max_over_ranks(e2e_s, device=dev)
+            e2e_s = max_over_ranks(e2e_s, device=red_dev)
         nbytes = B * H * S * D * 2
         e2e = {"value": job_flops / e2e_s / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes + 4 * B * H * S,
@@ -470,7 +478,10 @@ def run_ours(args):
         }
         if stub:
             line["stub"] = "orchestration test: CPU step, gloo, host clock (not a measurement)"
-        else:
+        if args.share_device:
+            line["shared_device"] = ("test mode: all ranks on cuda:0 over gloo "
+                                     "(not a scaling measurement)")
+        if not stub:
             line["kernel"] = {"name": "ta::sdpa_fwd_kernel<128,bf16>", "ctas": stats.ctas,
                               "block_m": stats.block_m, "block_n": stats.block_n,
                               "stages": stats.stages, "q_tiles_per_cta": stats.q_tiles_per_cta,
@@ -555,6 +566,8 @@ def main():
                     help="S of the CPU arms' one-head sample (default: the workload's)")
     ap.add_argument("--stub-step", action="store_true",
                     help="CPU orchestration test (gloo, stub step); not a measurement")
+    ap.add_argument("--share-device", action="store_true",
+                    help="GPU test mode: all ranks on cuda:0 over gloo; not a measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="all BASELINE configs (report only)")

@@ -77,3 +77,27 @@ def test_quantiles_match_reference_harness():
     xs = list(range(1, 21))
     assert bench.quantiles(xs) == (10.5, 19)
     assert bench.quantiles(list(range(1, 101))) == (50.5, 95)
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu(cuda_device):
+    # the multi-rank GPU flow (head shards, per-rank CUDA-event timing, max
+    # over ranks, e2e through the host entry, CPU baseline on rank 0, one
+    # JSON line) with two ranks sharing cuda:0 over gloo -- the box has one GPU
+    lines, r = _run_gpu("--gpus", "2", "--share-device")
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["heads_per_gpu"] == 32 and d["shared_device"]
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 4
+    assert d["cpu_baseline"]["value"] > 0
+
+
+def _run_gpu(*extra):
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "4", "--warmup", "3",
+                        "--cpu-sample-s", "512", *extra],
+                       capture_output=True, text=True, timeout=900, env=e, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return [ln for ln in r.stdout.splitlines() if ln.startswith("{")], r
