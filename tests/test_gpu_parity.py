@@ -577,3 +577,38 @@ def test_release_workspace_then_host_entry_again(ta, cuda_device):
         r = oracle_ref(q, k, v)
         assert np.abs(o.double().numpy() - r["o"]).max() <= TOL[O.F16]
         ta.release_workspace(0)
+
+
+# ------------------------------------------------------------ CUDA graphs
+@pytest.mark.parametrize("D,causal,padded,t_n", [(64, False, False, 128), (128, True, False, 128),
+                                                 (128, False, True, 64), (256, False, True, 128)])
+def test_device_entry_is_graph_capturable(ta, cuda_device, D, causal, padded, t_n):
+    # the device entry allocates nothing and never synchronises: it can be
+    # captured into a CUDA graph and replayed on new inputs in the same
+    # buffers (launch-bound serving shapes replay for the cost of one graph
+    # launch); padding lengths up to 32 batches travel in the parameters
+    import torch
+    B, H, S = 2, 3, 500
+    vl = [500, 123] if padded else None
+    sched = ta.TileSchedule(64, t_n, 2)
+    q, k, v = (torch.randn(B, H, S, D, device="cuda").bfloat16() for _ in range(3))
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, S, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up (plan cache, tensor-map memo)
+        ta.sdpa(q, k, v, causal=causal, valid_len=vl, out=o, return_lse=True, lse_out=lse,
+                schedule=sched)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ta.sdpa(q, k, v, causal=causal, valid_len=vl, out=o, return_lse=True, lse_out=lse,
+                schedule=sched)
+    for trial in range(3):
+        for x in (q, k, v):
+            x.copy_(torch.randn_like(x, dtype=torch.float32).bfloat16())
+        g.replay()
+        torch.cuda.synchronize()
+        ro, rl = ta.sdpa(q, k, v, causal=causal, valid_len=vl, return_lse=True, schedule=sched)
+        torch.cuda.synchronize()
+        assert torch.equal(o, ro) and torch.equal(lse, rl), trial
