@@ -104,7 +104,8 @@ typedef struct ta_kernel_stats {
  *   valid_len : HOST array of B entries, MaskKind::Padding only (else NULL);
  *             B <= 32 travels in the kernel parameters, larger B through a
  *             per-device pool of pinned/device slots (allocated on first
- *             use, reused once the launch that read a slot has completed)
+ *             use, reused once the launch that read a slot has completed;
+ *             not capturable in a CUDA graph: TA_ERR_UNSUPPORTED there)
  *   has_scale/scale : ScaleSpec (types.hpp:78-86); has_scale = 0 -> 1/sqrt(D)
  *   stats   : optional out-parameter (KernelStats analogue), may be NULL
  *

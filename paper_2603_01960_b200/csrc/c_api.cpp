@@ -401,6 +401,12 @@ ta_status run_device(const void* q, const void* k, const void* v, void* o, float
       for (int64_t b = 0; b < mask_args.batches; ++b)
         L.args.valid_len[b] = int(mask_args.valid_len[b]);
     } else {
+      // the pool's pinned staging and event queries cannot live in a CUDA
+      // graph (a replay would read whatever the slot holds then): refuse
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(cs, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+        return fail(TA_ERR_UNSUPPORTED,
+                    "padding masks with more than 32 batches cannot be captured in a CUDA graph");
       ta_status pst = padding_slot(size_t(mask_args.batches), &slot);
       if (pst != TA_OK) return pst;
       for (int64_t b = 0; b < mask_args.batches; ++b) slot->host[b] = int(mask_args.valid_len[b]);

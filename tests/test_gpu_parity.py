@@ -612,3 +612,18 @@ def test_device_entry_is_graph_capturable(ta, cuda_device, D, causal, padded, t_
         ro, rl = ta.sdpa(q, k, v, causal=causal, valid_len=vl, return_lse=True, schedule=sched)
         torch.cuda.synchronize()
         assert torch.equal(o, ro) and torch.equal(lse, rl), trial
+
+
+def test_large_batch_padding_refuses_graph_capture(ta, cuda_device):
+    # B > 32 padding lengths come from a host-staged pool: not capturable,
+    # and the library says so instead of recording a stale copy
+    import torch
+    B, H, S, D = 40, 1, 64, 64
+    q = torch.randn(B, H, S, D, device="cuda").bfloat16()
+    vl = [S] * B
+    ta.sdpa(q, q, q, valid_len=vl)  # outside a capture: fine
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(ta.UnsupportedScheduleError, match="captured"):
+        with torch.cuda.graph(g):
+            ta.sdpa(q, q, q, valid_len=vl)
