@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
@@ -1329,15 +1330,17 @@ cudaError_t launch_typed(const FwdLaunch& L) {
   using C = Cfg<D, kQT, kBN, kPair>;
   auto kern = L.args.trace != nullptr ? sdpa_fwd_kernel<D, kBF16, true, kQT, kBN, kPair>
                                       : sdpa_fwd_kernel<D, kBF16, false, kQT, kBN, kPair>;
-  static bool attr_set[64][2] = {};  // per device, per instantiation
+  // the dynamic shared-memory opt-in, once per device and instantiation
+  // (idempotent: concurrent first calls may both set it)
+  static std::atomic<bool> attr_set[64][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   const int tr = L.args.trace != nullptr;
-  if (dev < 64 && !attr_set[dev][tr]) {
+  if (dev >= 64 || !attr_set[dev][tr].load(std::memory_order_acquire)) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set[dev][tr] = true;
+    if (dev < 64) attr_set[dev][tr].store(true, std::memory_order_release);
   }
   const int rows_per_cta = kBM * kQT;
   int64_t qblocks = (L.args.seq_len + rows_per_cta - 1) / rows_per_cta;
@@ -1419,23 +1422,21 @@ cudaError_t launch_d64_persistent(const FwdLaunch& L) {
   constexpr int kSmem = 2 * Cfg<64, 1>::kTileBytes + Cfg<64, 1>::kSlots * Cfg<64, 1>::kTileBytes +
                         1024 /*barriers*/ + 1024 /*align pad*/;
   static_assert(sizeof(BarriersD64) <= 1024, "barrier block");
-  static bool attr_set[64][2] = {};
-  static int sms[64] = {};
+  static std::atomic<bool> attr_set[64][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   const int tr = L.args.trace != nullptr;
-  if (dev < 64 && !attr_set[dev][tr]) {
+  if (dev >= 64 || !attr_set[dev][tr].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
-    attr_set[dev][tr] = true;
+    if (dev < 64) attr_set[dev][tr].store(true, std::memory_order_release);
   }
-  if (dev < 64 && sms[dev] == 0) {
-    cudaError_t e = cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-  }
+  int sms = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
   const int64_t items = int64_t((L.args.seq_len + kBM - 1) / kBM) * L.bh;
   if (items > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
-  const int64_t slots = int64_t(dev < 64 ? sms[dev] : 148) * Roles<1>::kMinBlocks;
+  const int64_t slots = int64_t(sms) * Roles<1>::kMinBlocks;
   const unsigned grid = unsigned(items < slots ? items : slots);
   FwdArgs a = L.args;
   a.bh_count = int(L.bh);
