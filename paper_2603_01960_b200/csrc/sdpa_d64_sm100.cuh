@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(Roles<1>::kThreads, Roles<1>::kMinBlocks)
           mbar_wait_ctrl(smem_u32(&bars->p_full[g & 1][h]), uint32_t((g >> 1) & 1));
           tc_fence_after();
           constexpr int kSteps = kBN128 / 16 / kPParts;
-          static_assert(kSteps % 4 == 0, "P part = 4k K-steps");
+          // (value-dependent: checked only where the kernel is instantiated)
+          static_assert(kSteps % 4 == 0 || (kBF16 && !kBF16), "P part = 4k K-steps");
 #pragma unroll
           for (int q = 0; q < kSteps / 4; ++q) {
             const int ks0 = h * kSteps + q * 4;

@@ -1458,8 +1458,10 @@ cudaError_t launch_sdpa_fwd(const FwdLaunch& L) {
     return L.bf16 ? launch_typed<128, true>(L) : launch_typed<128, false>(L);
   }
   if (L.head_dim == 64) {
-    if constexpr (TA_D64_PERSIST != 0 && kQTilesFor<64> == 1 && TA_D64_ROT)
+#if TA_D64_PERSIST != 0  // (compiled only when selected)
+    if constexpr (kQTilesFor<64> == 1 && TA_D64_ROT)
       return L.bf16 ? launch_d64_persistent<true>(L) : launch_d64_persistent<false>(L);
+#endif
     return L.bf16 ? launch_typed<64, true>(L) : launch_typed<64, false>(L);
   }
   if (L.head_dim == 192) return L.bf16 ? launch_typed<192, true>(L) : launch_typed<192, false>(L);
