@@ -126,35 +126,47 @@ inline uint16_t to_bf16_bits(float f) {
   return uint16_t(u >> 16);
 }
 
+// float -> IEEE half bits, round to nearest even, integer-only (the harness
+// converts every element of q/k/v per call, so this sits on the host path)
 inline uint16_t to_f16_bits(float f) {
   uint32_t x;
   std::memcpy(&x, &f, 4);
   const uint16_t sign = uint16_t((x >> 16) & 0x8000u);
-  const float a = std::fabs(f);
-  if (std::isnan(f)) return uint16_t(sign | 0x7E00u);
-  if (a >= 65520.0f) return uint16_t(sign | 0x7C00u);
-  if (a < 0x1.0p-14f) return uint16_t(sign | uint16_t(std::nearbyint(double(a) * 0x1.0p24)));
-  int e;
-  double m = std::nearbyint(std::frexp(double(a), &e) * 2048.0);
-  if (m >= 2048.0) {
-    m /= 2.0;
-    ++e;
+  const uint32_t a = x & 0x7FFFFFFFu;
+  if (a > 0x7F800000u) return uint16_t(sign | 0x7E00u);   // NaN
+  if (a >= 0x477FF000u) return uint16_t(sign | 0x7C00u);  // |f| >= 65520 -> inf
+  if (a >= 0x38800000u) {  // normal half: rebias the exponent, round 13 bits
+    const uint32_t r = a - 0x38000000u;
+    return uint16_t(sign | ((r + 0xFFFu + ((r >> 13) & 1u)) >> 13));
   }
-  return uint16_t(sign | uint16_t((e + 14) << 10) | (uint16_t(m) & 0x3FFu));
+  if (a <= 0x33000000u) return sign;  // |f| <= 2^-25 -> 0 (the tie rounds to even)
+  // subnormal half: |f| * 2^24 rounded to nearest even (carries into the
+  // smallest normal on round-up from 0x3FF)
+  const uint32_t e = a >> 23, m = (a & 0x7FFFFFu) | 0x800000u;
+  const uint32_t shift = 126u - e;  // 14..24
+  const uint32_t q = m >> shift, rem = m & ((1u << shift) - 1u), half = 1u << (shift - 1u);
+  return uint16_t(sign | (q + ((rem > half || (rem == half && (q & 1u))) ? 1u : 0u)));
 }
 
 inline float from_bits(uint16_t h, DType dt) {
+  uint32_t u;
   if (dt == DType::BF16Emu) {
-    const uint32_t u = uint32_t(h) << 16;
-    float f;
-    std::memcpy(&f, &u, 4);
-    return f;
+    u = uint32_t(h) << 16;
+  } else {
+    const uint32_t sign = uint32_t(h & 0x8000u) << 16, ex = (h >> 10) & 0x1Fu, man = h & 0x3FFu;
+    if (ex == 31) {
+      u = sign | 0x7F800000u | (man << 13);  // inf / NaN
+    } else if (ex != 0) {
+      u = sign | ((ex + 112u) << 23) | (man << 13);
+    } else {
+      const float v = float(man) * 0x1.0p-24f;  // subnormal (exact)
+      std::memcpy(&u, &v, 4);
+      u |= sign;
+    }
   }
-  const uint32_t ex = (h >> 10) & 0x1Fu, man = h & 0x3FFu;
-  double v = ex == 0 ? std::ldexp(double(man), -24)
-           : ex == 31 ? (man ? NAN : INFINITY)
-                      : std::ldexp(double(man | 0x400u), int(ex) - 25);
-  return float((h & 0x8000u) ? -v : v);
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
 }
 
 [[noreturn]] inline void raise(ta_status st) {

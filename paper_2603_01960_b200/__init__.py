@@ -126,10 +126,14 @@ def lib() -> ctypes.CDLL:
     L.ta_device_supported.argtypes = [cint]
     L.ta_sdpa_check.restype = cint
     L.ta_sdpa_check.argtypes = [_Shape, cint, cint, vp, cint, dbl, _Schedule]
-    L.ta_release_workspace.restype = cint
-    L.ta_release_workspace.argtypes = [cint]
-    L.ta_debug_exp2.restype = cint
-    L.ta_debug_exp2.argtypes = [vp, vp, i64, cint, vp]
+    # (ABI 1 additions: bound when present, so older builds of the same ABI
+    # still load for A/B timing; tests/test_abi.py checks the product exports all)
+    if hasattr(L, "ta_release_workspace"):
+        L.ta_release_workspace.restype = cint
+        L.ta_release_workspace.argtypes = [cint]
+    if hasattr(L, "ta_debug_exp2"):
+        L.ta_debug_exp2.restype = cint
+        L.ta_debug_exp2.argtypes = [vp, vp, i64, cint, vp]
     L.ta_debug_umma_gemm.restype = cint
     L.ta_debug_umma_gemm.argtypes = [cint, cint, vp, vp, vp, vp]
     _lib = L

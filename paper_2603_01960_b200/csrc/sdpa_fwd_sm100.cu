@@ -578,29 +578,33 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           wait_full(0);
           issue_qk(0, 0, C::s_col(0));
           release(0);
-          for (int j = 0; j < n; ++j) {
-            if (j + 1 < n) {
-              // K_{j+1}'s ring position (written out: a constexpr helper
-              // call here changes nvcc's unrolling of this loop at D=64 and
-              // costs 100 spill instructions)
-              int rk = 2 * (j + 1);
-              if constexpr (C::kConsumeOrder) rk = 2 * j + 1;
-              mbar_wait_ctrl(smem_u32(&bars->s_read), uint32_t(j & 1));
-              tc_fence_after();
-              if (lane == 0) rec(kEvMmaWaitP1, j);  // (rotation traces: s_read(j) seen)
-              wait_full(rk);
-              if (lane == 0) rec(kEvMmaIssuedPV1, j);  // (... K_{j+1} landed)
-              issue_qk(0, rk, C::s_col(j + 1));
-              if (lane == 0) rec(kEvSm1PArrive, j);  // (... QK(j+1) issued)
-              release(rk);
-            }
+          for (int j = 0; j + 1 < n; ++j) {
+            // K_{j+1}'s ring position (written out: a constexpr helper
+            // call here changes nvcc's unrolling of this loop at D=64 and
+            // costs 100 spill instructions)
+            int rk = 2 * (j + 1);
+            if constexpr (C::kConsumeOrder) rk = 2 * j + 1;
+            mbar_wait_ctrl(smem_u32(&bars->s_read), uint32_t(j & 1));
+            tc_fence_after();
+            if (lane == 0) rec(kEvMmaWaitP1, j);  // (rotation traces: s_read(j) seen)
+            wait_full(rk);
+            if (lane == 0) rec(kEvMmaIssuedPV1, j);  // (... K_{j+1} landed)
+            issue_qk(0, rk, C::s_col(j + 1));
+            if (lane == 0) rec(kEvSm1PArrive, j);  // (... QK(j+1) issued)
+            release(rk);
             int rv = 2 * j + 1;  // V_j
-            if constexpr (C::kConsumeOrder) rv = j + 1 < n ? 2 * j + 2 : 2 * n - 1;
+            if constexpr (C::kConsumeOrder) rv = 2 * j + 2;
             wait_full(rv);
-            zero_v_tail(rv, j);
             issue_pv(0, rv, j > 0, j);
             release(rv);
           }
+          // the last V tile (peeled: the padding tail is zeroed outside the
+          // steady-state loop, whose code nvcc otherwise schedules worse)
+          const int rv = 2 * n - 1;
+          wait_full(rv);
+          zero_v_tail(rv, n - 1);
+          issue_pv(0, rv, n > 1, n - 1);
+          release(rv);
           umma_commit_warp(smem_u32(&bars->o_last));
         }
       } else if constexpr (kQT == 1) {
@@ -616,9 +620,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
           for (int j = 1; j < n; ++j) {
             // S(j) overwrites the S / P columns PV(j-1) reads: in-order
             // after it on the tensor pipe
+            // (V_{j-1} is never the padding tail: that is tile n - 1)
             const int rk = 2 * j, rv = 2 * j - 1;
             wait_full(rv);
-            zero_v_tail(rv, j - 1);
             issue_pv(0, rv, j > 1, j - 1);
             release(rv);
             wait_full(rk);
@@ -642,9 +646,9 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         issue_qk(1, 0);
         release(0);
         for (int j = 1; j < n1; ++j) {
+          // (V_{j-1} is never the padding tail: padding has n1 = n_kv_seq)
           const int rk = 2 * j, rv = 2 * j - 1;
           wait_full(rv);
-          zero_v_tail(rv, j - 1);
           if (j - 1 < n0) issue_pv(0, rv, j > 1, j - 1);
           wait_full(rk);
           if (j < n0) issue_qk(0, rk);

@@ -13,6 +13,8 @@ timeout 600 python scripts/tile_table.py $O/tile_table.md > $O/tile_table.log 2>
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ncu_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sdpa_fwd_kernel -s 3 -c 1 \
+  -o $O/prof_long python scripts/profile_case.py 8 64 32768 128 bf16 5 > $O/ncu_long.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sdpa_fwd_kernel -s 3 -c 1 \
   -o $O/prof_d256 python scripts/profile_case.py 8 32 4096 256 bf16 5 > $O/ncu_d256.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sdpa_fwd_kernel -s 3 -c 1 \
   -o $O/prof_d64 python scripts/profile_case.py 8 32 4096 64 bf16 5 > $O/ncu_d64.log 2>&1

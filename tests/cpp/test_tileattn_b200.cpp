@@ -106,6 +106,51 @@ static void test_unsupported_schedules_are_rejected() {  // test_tiled.cpp:256-2
   CHECK(cache.constructions() == 0);
 }
 
+// the host conversions the mirror applies to every element (harness inputs
+// are float): bit-exact round-to-nearest-even against a frexp/nearbyint
+// restatement on a strided sweep of every float bit pattern, and every half
+// round-trips through from_bits
+static uint16_t f16_bits_slow(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint16_t sign = uint16_t((x >> 16) & 0x8000u);
+  const float a = std::fabs(f);
+  if (std::isnan(f)) return uint16_t(sign | 0x7E00u);
+  if (a >= 65520.0f) return uint16_t(sign | 0x7C00u);
+  if (a < 0x1.0p-14f) return uint16_t(sign | uint16_t(std::nearbyint(double(a) * 0x1.0p24)));
+  int e;
+  double m = std::nearbyint(std::frexp(double(a), &e) * 2048.0);
+  if (m >= 2048.0) {
+    m /= 2.0;
+    ++e;
+  }
+  return uint16_t(sign | uint16_t((e + 14) << 10) | (uint16_t(m) & 0x3FFu));
+}
+
+static void test_host_f16_conversions() {
+  int bad = 0;
+  for (uint64_t i = 0; i < (uint64_t(1) << 32); i += 4093) {
+    const uint32_t u = uint32_t(i);
+    float f;
+    std::memcpy(&f, &u, 4);
+    bad += tileattn_b200::detail::to_f16_bits(f) != f16_bits_slow(f);
+  }
+  for (uint32_t u : {0x38800000u, 0x387FFFFFu, 0x33000000u, 0x33000001u, 0x477FEFFFu,
+                     0x477FF000u, 0x7F800000u, 0x7FC00000u, 0x80000000u, 0xB3800000u}) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    bad += tileattn_b200::detail::to_f16_bits(f) != f16_bits_slow(f);
+  }
+  CHECK(bad == 0);
+  int trip = 0;
+  for (uint32_t h = 0; h < 65536; ++h) {
+    if (((h >> 10) & 0x1Fu) == 31 && (h & 0x3FFu)) continue;  // NaN payloads
+    trip += tileattn_b200::detail::to_f16_bits(
+                tileattn_b200::detail::from_bits(uint16_t(h), DType::F16Emu)) != h;
+  }
+  CHECK(trip == 0);
+}
+
 static void test_validation_order_and_classes() {  // tiled.cpp:256-259, types.cpp:80-116
   PlanCache cache;
   AttnInput bad = make_input(Shape{1, 1, 32, 64}, DType::BF16Emu, 1);
@@ -249,6 +294,7 @@ int main(int argc, char** argv) {
   std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"unsupported schedules are rejected", test_unsupported_schedules_are_rejected},
       {"validation order and error classes", test_validation_order_and_classes},
+      {"host f16 conversions round to nearest even", test_host_f16_conversions},
   };
   if (!cpu_only) {
     cases.insert(cases.end(), {
