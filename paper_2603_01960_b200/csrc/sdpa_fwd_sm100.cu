@@ -183,7 +183,7 @@ struct Cfg {
   static constexpr int kSlots = D > 128 ? (D == 192 ? 3 : 2)
                                 : D == 128 ? (kQT == 1 ? 2 : TA_SLOTS_D128 * (128 / kBN) * (kPair ? 2 : 1))
                                 : kQT == 1 ? TA_SLOTS_D64 : 8;
-  static constexpr bool kSplit = kSplitFor<D, kQT, kBN> && !kPair;
+  static constexpr bool kSplit = kSplitFor<D, kQT, kBN>;
   static constexpr int kSmemData = kQT * kTileBytes + kSlots * kKVBytes;
   // (kSplit: + 4 KB of per-row exchange between the two warps of a row:
   // [max | l][Q tile][lane quadrant][column half][lane] floats)
@@ -237,7 +237,6 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
                     const __grid_constant__ CUtensorMap tmap_o, FwdArgs args) {
   using C = Cfg<D, kQT, kBN, kPair>;
   using R = RolesFor<D, kQT, kBN>;
-  static_assert(!kPair || !C::kSplit, "pair kernel: one softmax warp per row");
   constexpr int kWarpAlloc = R::kWarpAlloc, kWarpTma = R::kWarpTma, kWarpTrace = R::kWarpTrace,
                 kWarpMma = R::kWarpMma;
   // stale max at both head dims: it takes the row max (and its latency)
@@ -849,7 +848,12 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(pbar);
+      if (lane == 0) {
+        if constexpr (kPair)  // the leader's barrier (the MMA issuer waits there)
+          mbar_arrive_cluster(mapa_shared(pbar, 0));
+        else
+          mbar_arrive(pbar);
+      }
       if (tr) rec(kEvSm0PArrive + 5 * t, j);
       // warp skew of tile 0 (trace builds): W1 = the row partner (wq 0, c 1),
       // W2 / W3 = the two warps on the MMA warp's SMSP (wq 3, c 0 / 1)
@@ -1383,7 +1387,7 @@ constexpr bool kHasBN64 = kQTilesFor<128> == 2;
 #ifndef TA_PAIR
 #define TA_PAIR 0
 #endif
-constexpr bool kHasPair = TA_PAIR != 0 && kQTilesFor<128> == 2 && !TA_D128_SPLIT;
+constexpr bool kHasPair = TA_PAIR != 0 && kQTilesFor<128> == 2;
 
 bool fwd_use_pair(int64_t D, int block_n, int mask) {
   return kHasPair && D > 64 && D <= 128 && block_n == 128 && mask != kMaskCausal;
