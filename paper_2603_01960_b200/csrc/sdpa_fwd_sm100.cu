@@ -512,14 +512,24 @@ __global__ void __launch_bounds__(RolesFor<D, kQT, kBN>::kThreads, RolesFor<D, k
         if (args.mask != kMaskPadding || j != n_kv_seq - 1) return;
         const int r0 = kv_len - j * kBN;  // first masked key row of the tile
         if (r0 >= kBN) return;
-        constexpr int kVRegions = kPair ? 1 : C::kRegions;
         const uint32_t vbase = sring + slot_of(r) * C::kKVBytes;
-        for (int i = r0 * 8 + int(lane); i < kBN * 8; i += 32) {  // 16-B pieces
-          for (int g = 0; g < kVRegions; ++g)
-            st_shared_v4(vbase + g * C::kKVRegionBytes + (i >> 3) * 128 + (i & 7) * 16, 0u, 0u,
-                         0u, 0u);
+        if constexpr (kPair) {
+          // each CTA of the pair holds 64 of the V columns (one region): the
+          // leader's MMA warp zeroes the rows in both through shared::cluster
+          for (uint32_t cta = 0; cta < 2; ++cta) {
+            const uint32_t vb = mapa_shared(vbase, cta);
+            for (int i = r0 * 8 + int(lane); i < kBN * 8; i += 32)  // 16-B pieces
+              st_cluster_zero_v4(vb + (i >> 3) * 128 + (i & 7) * 16);
+          }
+          fence_proxy_async_cluster();
+        } else {
+          for (int i = r0 * 8 + int(lane); i < kBN * 8; i += 32) {  // 16-B pieces
+            for (int g = 0; g < C::kRegions; ++g)
+              st_shared_v4(vbase + g * C::kKVRegionBytes + (i >> 3) * 128 + (i & 7) * 16, 0u, 0u,
+                           0u, 0u);
+          }
+          fence_proxy_async_smem();  // generic-proxy writes before the tensor core reads
         }
-        fence_proxy_async_smem();  // generic-proxy writes before the tensor core reads
         __syncwarp();
       };
       auto issue_pv = [&](int t, int r, bool accumulate, int j) {
